@@ -1,0 +1,50 @@
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+GOLDEN = Path(__file__).resolve().parent / "golden"
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) and the built CUDA library")
+    config.addinivalue_line("markers", "slow: long-running CPU test")
+
+
+def load_golden(name: str):
+    return np.load(GOLDEN / name, allow_pickle=False)
+
+
+@pytest.fixture(scope="session")
+def ref_fixtures():
+    return load_golden("reference_fixtures.npz")
+
+
+@pytest.fixture(scope="session")
+def tiny_golden():
+    return load_golden("tiny_pipeline.npz")
+
+
+@pytest.fixture(scope="session")
+def cfg1_golden():
+    return load_golden("cfg1_pipeline.npz")
+
+
+@pytest.fixture(scope="session")
+def large_golden():
+    return load_golden("large_masks.npz")
+
+
+def tiny_case(g, i):
+    """Unpack one tiny golden case: (inputs, meta dict)."""
+    seed, t_v, t_t, d, block, is64, f, p, r, force = g[f"c{i}_meta"].tolist()
+    meta = dict(seed=int(seed), t_v=int(t_v), t_t=int(t_t), d=int(d), block=int(block),
+                f=float(f), p=float(p), r=int(r), force=bool(force))
+    return (g[f"c{i}_qv"], g[f"c{i}_qt"], g[f"c{i}_k"], g[f"c{i}_v"]), meta
+
+
+N_TINY = 10
