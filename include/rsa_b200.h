@@ -1,0 +1,170 @@
+/*
+ * rsa_b200.h -- C ABI of the B200-native Rectified SpaAttn hot path.
+ *
+ * One call = the reference's `rectified_attention_pipeline(problem, config,
+ * variant)` (reference: pkg/src/rectattn/rectify.py:107-176) for H independent
+ * single-head problems at once.  Plain pointers and sizes only: no torch types.
+ *
+ * Memory: every pointer is a DEVICE pointer owned by the caller.  Q, K, V and
+ * O are [heads][T][d] with T = t_video + t_text; rows [0, t_video) are video
+ * tokens and rows [t_video, T) text tokens (reference core.py:6-8).
+ * The library never allocates device memory: callers size the workspace with
+ * rsa_workspace_size() and pass it in.  All work is enqueued on `stream`; no
+ * call synchronises except rsa_check_device_status().
+ *
+ * Errors: every entry point returns an rsa_status whose values map 1:1 onto
+ * the reference's exception classes (pkg/src/rectattn/errors.py:4-45); the
+ * thread-local rsa_last_error() holds the message.
+ */
+#ifndef RSA_B200_H
+#define RSA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  RSA_OK = 0,
+  RSA_ERR_SHAPE = 1,            /* ShapeError          errors.py:8-9   */
+  RSA_ERR_BLOCK_SIZE = 2,       /* BlockSizeError      errors.py:12-13 */
+  RSA_ERR_EMPTY_ROW = 3,        /* EmptyRowError       errors.py:16-17 */
+  RSA_ERR_CONFIG = 4,           /* ConfigError         errors.py:28-29 */
+  RSA_ERR_DEGENERATE_ROW = 5,   /* DegenerateRowError  errors.py:24-25 */
+  RSA_ERR_CUDA = 6,             /* CUDA runtime / launch failure       */
+  RSA_ERR_UNSUPPORTED = 7       /* shape outside the compiled kernels  */
+} rsa_status;
+
+typedef enum { RSA_BF16 = 0, RSA_F32 = 1, RSA_F64 = 2 } rsa_dtype;
+
+/* Reference VARIANTS, rectify.py:23-24, in the same order. */
+typedef enum {
+  RSA_VARIANT_FULL = 0,
+  RSA_VARIANT_SPARSE_UNRECTIFIED = 1,
+  RSA_VARIANT_SPARSE_RECTIFIED = 2,
+  RSA_VARIANT_SPARSE_RECTIFIED_NO_GAPR = 3,
+  RSA_VARIANT_COMPENSATE_ALL = 4
+} rsa_variant;
+
+/* Attention kernel selection (K3). AUTO picks the tcgen05 kernel for bf16 and
+ * block/head_dim in {64,128}, the CUDA-core kernel otherwise. */
+typedef enum { RSA_KERNEL_AUTO = 0, RSA_KERNEL_TCGEN05 = 1, RSA_KERNEL_SIMT = 2 } rsa_kernel;
+
+typedef struct {
+  int64_t heads;        /* independent (batch, head) problems                */
+  int64_t t_video;      /* T_v, must be a multiple of block (core.py:71-72)    */
+  int64_t t_text;       /* T_t >= 0                                          */
+  int64_t head_dim;     /* d                                                 */
+  int64_t block;        /* B: query and key block size                       */
+  int32_t dtype;        /* rsa_dtype of Q/K/V/O                              */
+  int32_t kernel;       /* rsa_kernel                                        */
+} rsa_shape;
+
+/* SparsityConfig (masks.py:21-41) + variant (rectify.py:23-24). */
+typedef struct {
+  double top_k_fraction;     /* f in (0, 1]                 */
+  double weight_threshold;   /* p in [0, 1]                 */
+  int32_t adjacency_radius;  /* r >= 0                      */
+  int32_t force_text_blocks; /* bool                        */
+  int32_t variant;           /* rsa_variant                 */
+  int32_t reserved;
+} rsa_config;
+
+/* Block grid (core.py:94-123 BlockGrid): N query blocks, M kv blocks. */
+typedef struct {
+  int64_t n_q;
+  int64_t n_kv;
+  int64_t n_text_blocks;
+  int64_t last_text_block_len;
+  int64_t n_cols;            /* N + T_t + n_text: columns of the score matrix */
+} rsa_grid;
+
+/* Byte offsets of the intermediate results inside the workspace.  Every array
+ * is [heads][...] row-major.  fp64 unless noted. */
+typedef struct {
+  size_t q_pool;      /* [N][d]        pooled video queries   (core.py:192-201)   */
+  size_t q_def;       /* [N][d]        q_sums - B*q_pool      (masks.py:165-166)   */
+  size_t k_cat;       /* [n_cols][d]   k_v_pool ; raw text keys ; pooled text keys  */
+  size_t k_def;       /* [M][d]        k_sums - len*k_pool    (masks.py:170-171)   */
+  size_t v_pool;      /* [M][d]        pooled values          (core.py:198)        */
+  size_t scores;      /* [N][n_cols]   q_pool.k_cat / sqrt(d) (ipar.py:41, masks.py:127) */
+  size_t a_pool;      /* [N][M]        implicit full attention (ipar.py:69-86)     */
+  size_t mask_bits;   /* u8 [N][M]: bit0 mask, bit1 importance, bit2 gain>error,
+                         bit3 adjacency, bit4 applied compensation                 */
+  size_t r;           /* [N]           rectification factors  (rectify.py:56-63) */
+  size_t r_eff;       /* f32 [N]       factor the epilogue applies (1 if unrectified) */
+  size_t comp;        /* [N][d]        sum_applied a_pool v_pool (rectify.py:84-87) */
+  size_t kv_count;    /* i32 [N]       retained kv blocks per query block           */
+  size_t kv_list;     /* i32 [N][M]    ascending retained kv block ids               */
+  size_t tile_count;  /* i32 [tiles]   kv entries per 128-row tcgen05 tile           */
+  size_t tile_list;   /* i32 [tiles][M] (kv id | member bits << 24)                  */
+  size_t status;      /* i32 [4]       device status flags (degenerate row, ...)     */
+  size_t total;
+} rsa_workspace_layout;
+
+/* Validation + block grid; RSA_ERR_* mirrors AttentionProblem.__post_init__
+ * (core.py:59-80) and SparsityConfig.__post_init__ (masks.py:35-41). */
+rsa_status rsa_plan(const rsa_shape* shape, const rsa_config* cfg, rsa_grid* grid);
+rsa_status rsa_workspace_layout_query(const rsa_shape* shape, rsa_workspace_layout* layout);
+size_t rsa_workspace_size(const rsa_shape* shape);
+
+/* K1: exactly rounded fp64 block pooling of Q_video, K (video / text blocks
+ * isolated) and V.  Replaces pool_problem + block_sums (core.py:154-201,
+ * masks.py:130-135, masks.py:165-171). */
+rsa_status rsa_pool(const rsa_shape* shape, const void* q, const void* k, const void* v,
+                    void* workspace, void* stream);
+
+/* K2: fp64 pooled scoring, IPAR reallocation, deterministic top-k/threshold
+ * selection, gain/error gate, rectification factors and compensation rows.
+ * Replaces implicit_full_attention (ipar.py:69-86), build_sparse_mask
+ * (masks.py:83-117), gain_error/compensation_mask (masks.py:120-219) and
+ * rectification_factors (rectify.py:56-63).  Needs rsa_pool first. */
+rsa_status rsa_select(const rsa_shape* shape, const rsa_config* cfg, void* workspace,
+                      void* stream);
+
+/* K3+K4: block-sparse flash attention over the retained kv blocks with the
+ * IPAR rescale and GAPR compensation fused into the epilogue, plus full
+ * attention for the text queries.  Replaces block_sparse_attention
+ * (kernel.py:65-117), text_full_attention (kernel.py:120-145) and
+ * apply_rectification (rectify.py:66-89).  `lse` (f32 [heads][T], natural
+ * log, may be NULL) is the reference's row_log_denominators. Needs rsa_select. */
+rsa_status rsa_attention(const rsa_shape* shape, const rsa_config* cfg, const void* q,
+                         const void* k, const void* v, void* out, float* lse,
+                         void* workspace, void* stream);
+
+/* K1 -> K2 -> K3+K4: the whole pipeline (rectify.py:107-176). */
+rsa_status rsa_forward(const rsa_shape* shape, const rsa_config* cfg, const void* q,
+                       const void* k, const void* v, void* out, float* lse,
+                       void* workspace, void* stream);
+
+/* Kernel-only seam (kernel.py:65-117): video queries over an explicit block
+ * mask (u8 [heads][N][M], nonzero = retained); no rectification.  Text rows
+ * of `out` are left untouched. */
+rsa_status rsa_block_sparse_attention(const rsa_shape* shape, const void* q, const void* k,
+                                      const void* v, const uint8_t* block_mask, void* out,
+                                      float* lse, void* workspace, void* stream);
+
+/* Kernel-only seam (kernel.py:120-145): `n_queries` text queries attend over
+ * all `n_keys` keys, tiled by `block` (last tile ragged).  q/out are
+ * [heads][n_queries][d], k/v [heads][n_keys][d]; `workspace` is unused. */
+rsa_status rsa_text_full_attention(int64_t heads, int64_t n_queries, int64_t n_keys,
+                                   int64_t head_dim, int64_t block, int32_t dtype, const void* q,
+                                   const void* k, const void* v, void* out, float* lse,
+                                   void* workspace, void* stream);
+
+/* Synchronises `stream` and converts device-side status flags (e.g. a
+ * reallocation denominator <= 0, ipar.py:62-64) into an rsa_status. */
+rsa_status rsa_check_device_status(void* workspace, void* stream);
+
+/* Number of kernel launches the last rsa_forward/rsa_attention enqueued. */
+int32_t rsa_last_launch_count(void);
+const char* rsa_last_error(void);
+const char* rsa_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RSA_B200_H */

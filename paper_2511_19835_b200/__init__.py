@@ -1,0 +1,29 @@
+"""B200-native Rectified SpaAttn (arXiv 2511.19835) hot path.
+
+Drop-in for the reference package ``rectattn``'s attention entry points
+(pkg/src/rectattn/__init__.py:4-24): the same containers, configuration,
+variants and exceptions, backed by four hand-written sm_100a stages in
+``librsa_b200.so`` (pool -> select -> block-sparse attention with the IPAR/GAPR
+rectification epilogue).  There is no CPU fallback.
+"""
+
+from .core import (VARIANTS, AttentionOutput, AttentionProblem, BlockGrid, CompensationMask,
+                   ImplicitAttention, PipelineAccounting, PipelineResult, PooledSet,
+                   RectificationFactors, SparseMask, SparsityConfig, check_result_invariants,
+                   partition, sparsity_and_flops)
+from .errors import (BlockSizeError, ConfigError, DegenerateRowError, EmptyRowError, IoError,
+                     MissingGridError, NativeError, RectAttnError, SchemaError, ShapeError,
+                     ZeroReferenceError, ZeroVectorError)
+
+__version__ = "0.1.0"
+
+_LAZY = {"rectified_attention_pipeline", "block_sparse_attention", "text_full_attention",
+         "rectified_sparse_attention"}
+
+
+def __getattr__(name):
+    # the pipeline module imports torch; keep `import paper_2511_19835_b200` light
+    if name in _LAZY:
+        from . import pipeline
+        return getattr(pipeline, name)
+    raise AttributeError(name)

@@ -1,0 +1,317 @@
+// extern "C" entry points of librsa_b200.so (include/rsa_b200.h).
+//
+// Host-side validation mirrors the reference's eager checks:
+//   AttentionProblem.__post_init__  core.py:59-80   (ShapeError, BlockSizeError)
+//   partition                       core.py:140-151 (N, M, ragged last text block)
+//   SparsityConfig.__post_init__    masks.py:35-41  (ConfigError)
+//   rectified_attention_pipeline    rectify.py:118-119 (unknown variant -> ConfigError)
+// and orchestrates K1 -> K2 -> K3 on the caller's stream with the caller's
+// workspace (no allocation, no synchronisation).
+#include "rsa_internal.cuh"
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+namespace {
+
+thread_local std::string g_last_error;
+thread_local int g_launches = 0;
+
+rsa_status fail(rsa_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+
+rsa_status cuda_fail(cudaError_t e, const char* where) {
+  return fail(RSA_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+rsa_status make_geometry(const rsa_shape* s, rsa::Geometry* g) {
+  if (!s) return fail(RSA_ERR_SHAPE, "null shape");
+  if (s->dtype < RSA_BF16 || s->dtype > RSA_F64)
+    return fail(RSA_ERR_SHAPE, "q/k/v must be bfloat16, float32 or float64");
+  if (s->heads < 1) return fail(RSA_ERR_SHAPE, "heads must be >= 1");
+  if (s->head_dim < 1) return fail(RSA_ERR_SHAPE, "head_dim must be >= 1");
+  if (s->t_video < 0 || s->t_text < 0) return fail(RSA_ERR_SHAPE, "token counts must be >= 0");
+  if (s->block <= 0)
+    return fail(RSA_ERR_BLOCK_SIZE, "block size must be positive, got " + std::to_string(s->block));
+  if (s->t_video % s->block != 0)
+    return fail(RSA_ERR_BLOCK_SIZE, "T_v=" + std::to_string(s->t_video) +
+                                        " is not divisible by block size " + std::to_string(s->block));
+  if (s->t_video == 0) return fail(RSA_ERR_SHAPE, "T_v must be >= 1 block");
+  g->H = s->heads;
+  g->Tv = s->t_video;
+  g->Tt = s->t_text;
+  g->T = s->t_video + s->t_text;
+  g->d = s->head_dim;
+  g->B = s->block;
+  g->N = s->t_video / s->block;
+  g->n_text = (s->t_text + s->block - 1) / s->block;
+  g->M = g->N + g->n_text;
+  g->last_len = g->n_text ? s->t_text - (g->n_text - 1) * s->block : 0;
+  g->n_cols = g->N + g->Tt + g->n_text;
+  g->dtype = s->dtype;
+  g->qt_rows = g->Tt;
+  g->qt_row0 = g->Tv;
+  g->q_rows = g->T;
+  const int64_t dmax = s->dtype == RSA_F64 ? 128 : 256;
+  if (g->d > dmax)
+    return fail(RSA_ERR_UNSUPPORTED, "head_dim " + std::to_string(g->d) + " > " + std::to_string(dmax));
+  if (g->M > 8192) return fail(RSA_ERR_UNSUPPORTED, "more than 8192 kv blocks");
+  return RSA_OK;
+}
+
+rsa_status check_config(const rsa_config* c) {
+  if (!c) return fail(RSA_ERR_CONFIG, "null config");
+  if (!(c->top_k_fraction > 0.0 && c->top_k_fraction <= 1.0))
+    return fail(RSA_ERR_CONFIG, "top_k_fraction must be in (0, 1], got " + std::to_string(c->top_k_fraction));
+  if (!(c->weight_threshold >= 0.0 && c->weight_threshold <= 1.0))
+    return fail(RSA_ERR_CONFIG, "weight_threshold must be in [0, 1], got " + std::to_string(c->weight_threshold));
+  if (c->adjacency_radius < 0)
+    return fail(RSA_ERR_CONFIG, "adjacency_radius must be >= 0, got " + std::to_string(c->adjacency_radius));
+  if (c->variant < RSA_VARIANT_FULL || c->variant > RSA_VARIANT_COMPENSATE_ALL)
+    return fail(RSA_ERR_CONFIG, "unknown variant " + std::to_string(c->variant));
+  return RSA_OK;
+}
+
+int64_t tiles_per_head(const rsa::Geometry& g) {
+  const int64_t G = (g.B <= rsa::kTcTileRows && rsa::kTcTileRows % g.B == 0) ? rsa::kTcTileRows / g.B : 1;
+  return (g.N + G - 1) / G;
+}
+
+void layout_of(const rsa::Geometry& g, rsa_workspace_layout* L) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes); return o; };
+  const size_t H = g.H, N = g.N, M = g.M, d = g.d, C = g.n_cols, TT = tiles_per_head(g);
+  L->status = take(64);
+  L->q_pool = take(H * N * d * 8);
+  L->q_def = take(H * N * d * 8);
+  L->k_cat = take(H * C * d * 8);
+  L->k_def = take(H * M * d * 8);
+  L->v_pool = take(H * M * d * 8);
+  L->scores = take(H * N * C * 8);
+  L->a_pool = take(H * N * M * 8);
+  L->mask_bits = take(H * N * M);
+  L->r = take(H * N * 8);
+  L->r_eff = take(H * N * 4);
+  L->comp = take(H * N * d * 8);
+  L->kv_count = take(H * N * 4);
+  L->kv_list = take(H * N * M * 4);
+  L->tile_count = take(H * TT * 4);
+  L->tile_list = take(H * TT * M * 4);
+  L->total = off;
+}
+
+rsa::Workspace bind(const rsa::Geometry& g, void* base) {
+  rsa_workspace_layout L;
+  layout_of(g, &L);
+  char* b = static_cast<char*>(base);
+  rsa::Workspace w;
+  w.status = reinterpret_cast<int32_t*>(b + L.status);
+  w.q_pool = reinterpret_cast<double*>(b + L.q_pool);
+  w.q_def = reinterpret_cast<double*>(b + L.q_def);
+  w.k_cat = reinterpret_cast<double*>(b + L.k_cat);
+  w.k_def = reinterpret_cast<double*>(b + L.k_def);
+  w.v_pool = reinterpret_cast<double*>(b + L.v_pool);
+  w.scores = reinterpret_cast<double*>(b + L.scores);
+  w.a_pool = reinterpret_cast<double*>(b + L.a_pool);
+  w.mask_bits = reinterpret_cast<uint8_t*>(b + L.mask_bits);
+  w.r = reinterpret_cast<double*>(b + L.r);
+  w.r_eff = reinterpret_cast<float*>(b + L.r_eff);
+  w.comp = reinterpret_cast<double*>(b + L.comp);
+  w.kv_count = reinterpret_cast<int32_t*>(b + L.kv_count);
+  w.kv_list = reinterpret_cast<int32_t*>(b + L.kv_list);
+  w.tile_count = reinterpret_cast<int32_t*>(b + L.tile_count);
+  w.tile_list = reinterpret_cast<int32_t*>(b + L.tile_list);
+  return w;
+}
+
+bool use_tc(const rsa_shape* s, const rsa::Geometry& g) {
+  if (s->kernel == RSA_KERNEL_SIMT) return false;
+  return rsa::tc_supported(g);
+}
+
+rsa_status run_attention(const rsa_shape* s, const rsa::Geometry& g, const rsa::Workspace& ws,
+                         const void* q, const void* k, const void* v, void* out, float* lse,
+                         bool rectify, bool text, cudaStream_t st) {
+  cudaError_t e;
+  const bool tc = use_tc(s, g);
+  if (s->kernel == RSA_KERNEL_TCGEN05 && !tc)
+    return fail(RSA_ERR_UNSUPPORTED, "tcgen05 kernel needs bf16 and block, head_dim in {64, 128}");
+  if (tc) {
+    e = rsa::launch_tile_lists(g, ws, st, &g_launches);
+    if (e != cudaSuccess) return cuda_fail(e, "tile_lists");
+    e = rsa::launch_attn_tc(g, q, k, v, out, lse, ws, rectify, text, st, &g_launches);
+    if (e != cudaSuccess) return cuda_fail(e, "attn_tc");
+  } else {
+    e = rsa::launch_attn_simt(g, q, k, v, out, lse, ws, rectify, false, st, &g_launches);
+    if (e != cudaSuccess) return cuda_fail(e, "attn_simt(video)");
+    if (text && g.Tt > 0) {
+      e = rsa::launch_attn_simt(g, q, k, v, out, lse, ws, false, true, st, &g_launches);
+      if (e != cudaSuccess) return cuda_fail(e, "attn_simt(text)");
+    }
+  }
+  return RSA_OK;
+}
+
+bool rectifies(int variant) {
+  return variant == RSA_VARIANT_SPARSE_RECTIFIED || variant == RSA_VARIANT_SPARSE_RECTIFIED_NO_GAPR ||
+         variant == RSA_VARIANT_COMPENSATE_ALL;
+}
+
+}  // namespace
+
+extern "C" {
+
+rsa_status rsa_plan(const rsa_shape* shape, const rsa_config* cfg, rsa_grid* grid) {
+  rsa::Geometry g;
+  rsa_status s = make_geometry(shape, &g);
+  if (s != RSA_OK) return s;
+  if (cfg) {
+    s = check_config(cfg);
+    if (s != RSA_OK) return s;
+  }
+  if (grid) {
+    grid->n_q = g.N;
+    grid->n_kv = g.M;
+    grid->n_text_blocks = g.n_text;
+    grid->last_text_block_len = g.last_len;
+    grid->n_cols = g.n_cols;
+  }
+  return RSA_OK;
+}
+
+rsa_status rsa_workspace_layout_query(const rsa_shape* shape, rsa_workspace_layout* layout) {
+  rsa::Geometry g;
+  rsa_status s = make_geometry(shape, &g);
+  if (s != RSA_OK) return s;
+  layout_of(g, layout);
+  return RSA_OK;
+}
+
+size_t rsa_workspace_size(const rsa_shape* shape) {
+  rsa_workspace_layout L;
+  if (rsa_workspace_layout_query(shape, &L) != RSA_OK) return 0;
+  return L.total;
+}
+
+rsa_status rsa_pool(const rsa_shape* shape, const void* q, const void* k, const void* v,
+                    void* workspace, void* stream) {
+  rsa::Geometry g;
+  rsa_status s = make_geometry(shape, &g);
+  if (s != RSA_OK) return s;
+  if (!q || !k || !v || !workspace) return fail(RSA_ERR_SHAPE, "null pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  rsa::Workspace ws = bind(g, workspace);
+  cudaError_t e = cudaMemsetAsync(ws.status, 0, 64, st);
+  if (e != cudaSuccess) return cuda_fail(e, "memset status");
+  e = rsa::launch_pool(g, q, k, v, ws, st, &g_launches);
+  if (e != cudaSuccess) return cuda_fail(e, "pool");
+  return RSA_OK;
+}
+
+rsa_status rsa_select(const rsa_shape* shape, const rsa_config* cfg, void* workspace, void* stream) {
+  rsa::Geometry g;
+  rsa_status s = make_geometry(shape, &g);
+  if (s != RSA_OK) return s;
+  s = check_config(cfg);
+  if (s != RSA_OK) return s;
+  if (!workspace) return fail(RSA_ERR_SHAPE, "null workspace");
+  // k_floor = math.ceil(top_k_fraction * M) (masks.py:100), IEEE double on the host
+  const int64_t k_floor = (int64_t)std::ceil(cfg->top_k_fraction * (double)g.M);
+  rsa::Workspace ws = bind(g, workspace);
+  cudaError_t e = rsa::launch_select(g, *cfg, k_floor, ws, static_cast<cudaStream_t>(stream), &g_launches);
+  if (e != cudaSuccess) return cuda_fail(e, "select");
+  return RSA_OK;
+}
+
+rsa_status rsa_attention(const rsa_shape* shape, const rsa_config* cfg, const void* q,
+                         const void* k, const void* v, void* out, float* lse, void* workspace,
+                         void* stream) {
+  rsa::Geometry g;
+  rsa_status s = make_geometry(shape, &g);
+  if (s != RSA_OK) return s;
+  s = check_config(cfg);
+  if (s != RSA_OK) return s;
+  if (!q || !k || !v || !out || !workspace) return fail(RSA_ERR_SHAPE, "null pointer");
+  rsa::Workspace ws = bind(g, workspace);
+  return run_attention(shape, g, ws, q, k, v, out, lse, rectifies(cfg->variant), true,
+                       static_cast<cudaStream_t>(stream));
+}
+
+rsa_status rsa_forward(const rsa_shape* shape, const rsa_config* cfg, const void* q, const void* k,
+                       const void* v, void* out, float* lse, void* workspace, void* stream) {
+  g_launches = 0;
+  rsa_status s = rsa_pool(shape, q, k, v, workspace, stream);
+  if (s != RSA_OK) return s;
+  s = rsa_select(shape, cfg, workspace, stream);
+  if (s != RSA_OK) return s;
+  return rsa_attention(shape, cfg, q, k, v, out, lse, workspace, stream);
+}
+
+rsa_status rsa_block_sparse_attention(const rsa_shape* shape, const void* q, const void* k,
+                                      const void* v, const uint8_t* block_mask, void* out,
+                                      float* lse, void* workspace, void* stream) {
+  g_launches = 0;
+  rsa::Geometry g;
+  rsa_status s = make_geometry(shape, &g);
+  if (s != RSA_OK) return s;
+  if (!q || !k || !v || !block_mask || !out || !workspace) return fail(RSA_ERR_SHAPE, "null pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  rsa::Workspace ws = bind(g, workspace);
+  cudaError_t e = cudaMemsetAsync(ws.status, 0, 64, st);
+  if (e != cudaSuccess) return cuda_fail(e, "memset status");
+  e = rsa::launch_lists_from_mask(g, block_mask, ws, st, &g_launches);
+  if (e != cudaSuccess) return cuda_fail(e, "lists_from_mask");
+  return run_attention(shape, g, ws, q, k, v, out, lse, false, false, st);
+}
+
+rsa_status rsa_text_full_attention(int64_t heads, int64_t n_queries, int64_t n_keys,
+                                   int64_t head_dim, int64_t block, int32_t dtype, const void* q,
+                                   const void* k, const void* v, void* out, float* lse,
+                                   void* workspace, void* stream) {
+  g_launches = 0;
+  if (block <= 0) return fail(RSA_ERR_BLOCK_SIZE, "block size must be positive");
+  if (n_keys < 1) return fail(RSA_ERR_SHAPE, "need at least one key row");
+  // keys tiled by `block` from row 0 (kernel.py:138): full tiles as "video"
+  // blocks, the remainder as one ragged trailing block
+  rsa_shape s{heads, (n_keys / block) * block, n_keys % block, head_dim, block, dtype, RSA_KERNEL_SIMT};
+  rsa::Geometry g;
+  g.H = heads; g.Tv = s.t_video; g.Tt = s.t_text; g.T = n_keys; g.d = head_dim; g.B = block;
+  g.N = g.Tv / block; g.n_text = g.Tt > 0 ? 1 : 0; g.M = g.N + g.n_text;
+  g.last_len = g.Tt; g.n_cols = 0; g.dtype = dtype;
+  g.qt_rows = n_queries; g.qt_row0 = 0; g.q_rows = n_queries;
+  if (dtype < RSA_BF16 || dtype > RSA_F64) return fail(RSA_ERR_SHAPE, "bad dtype");
+  if (head_dim < 1 || head_dim > (dtype == RSA_F64 ? 128 : 256))
+    return fail(RSA_ERR_UNSUPPORTED, "head_dim out of range");
+  if (n_queries == 0) return RSA_OK;
+  rsa::Workspace ws;
+  memset(&ws, 0, sizeof(ws));
+  (void)workspace;
+  cudaError_t e = rsa::launch_attn_simt(g, q, k, v, out, lse, ws, false, true,
+                                        static_cast<cudaStream_t>(stream), &g_launches);
+  if (e != cudaSuccess) return cuda_fail(e, "attn_simt(text)");
+  return RSA_OK;
+}
+
+rsa_status rsa_check_device_status(void* workspace, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int32_t flags[4] = {0, 0, 0, 0};
+  cudaError_t e = cudaMemcpyAsync(flags, workspace, sizeof(flags), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "status readback");
+  if (flags[rsa::ST_DEGENERATE])
+    return fail(RSA_ERR_DEGENERATE_ROW, "reallocation denominator is zero on some rows");
+  if (flags[rsa::ST_EMPTY_ROW]) return fail(RSA_ERR_EMPTY_ROW, "a mask row retains no key block");
+  return RSA_OK;
+}
+
+int32_t rsa_last_launch_count(void) { return g_launches; }
+const char* rsa_last_error(void) { return g_last_error.c_str(); }
+const char* rsa_version(void) { return "rsa_b200 0.1.0 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,83 @@
+// Internal declarations shared by the sm_100a kernels of librsa_b200.so.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <string>
+
+#include "../../include/rsa_b200.h"
+
+namespace rsa {
+
+// Device pointers into the caller's workspace (see rsa_workspace_layout).
+struct Workspace {
+  double* q_pool;
+  double* q_def;
+  double* k_cat;
+  double* k_def;
+  double* v_pool;
+  double* scores;
+  double* a_pool;
+  uint8_t* mask_bits;
+  double* r;
+  float* r_eff;
+  double* comp;
+  int32_t* kv_count;
+  int32_t* kv_list;
+  int32_t* tile_count;
+  int32_t* tile_list;
+  int32_t* status;
+};
+
+// Problem geometry resolved on the host (rsa_plan).
+struct Geometry {
+  int64_t H, Tv, Tt, T, d, B;
+  int64_t N, M, n_text, last_len, n_cols;
+  int dtype;
+  // text-query layout (text_full_attention may have any query count):
+  // text query i of head h is row qt_row0 + i of a [H][q_rows][d] buffer
+  int64_t qt_rows, qt_row0, q_rows;
+};
+
+enum MaskBit : uint8_t {
+  BIT_MASK = 1, BIT_IMPORTANCE = 2, BIT_COMP = 4, BIT_ADJ = 8, BIT_APPLIED = 16
+};
+
+enum StatusFlag { ST_DEGENERATE = 0, ST_EMPTY_ROW = 1, ST_DEFICIT = 2 };
+
+constexpr int kTcTileRows = 128;   // query rows per tcgen05 tile (UMMA M)
+
+// ---- dtype helpers ---------------------------------------------------------
+template <typename T> struct Acc { using type = float; };
+template <> struct Acc<double> { using type = double; };
+
+__device__ __forceinline__ float to_f32(__nv_bfloat16 x) { return __bfloat162float(x); }
+__device__ __forceinline__ float to_f32(float x) { return x; }
+__device__ __forceinline__ double to_f64(__nv_bfloat16 x) { return (double)__bfloat162float(x); }
+__device__ __forceinline__ double to_f64(float x) { return (double)x; }
+__device__ __forceinline__ double to_f64(double x) { return x; }
+
+template <typename T> __device__ __forceinline__ T from_acc(float x);
+template <> __device__ __forceinline__ __nv_bfloat16 from_acc<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
+template <> __device__ __forceinline__ float from_acc<float>(float x) { return x; }
+template <typename T> __device__ __forceinline__ T from_acc(double x) { return (T)x; }
+
+// ---- launchers (one per .cu file) -----------------------------------------
+cudaError_t launch_pool(const Geometry& g, const void* q, const void* k, const void* v,
+                        const Workspace& ws, cudaStream_t st, int* launches);
+cudaError_t launch_select(const Geometry& g, const rsa_config& cfg, int64_t k_floor,
+                          const Workspace& ws, cudaStream_t st, int* launches);
+cudaError_t launch_lists_from_mask(const Geometry& g, const uint8_t* mask,
+                                   const Workspace& ws, cudaStream_t st, int* launches);
+cudaError_t launch_tile_lists(const Geometry& g, const Workspace& ws, cudaStream_t st,
+                              int* launches);
+cudaError_t launch_attn_simt(const Geometry& g, const void* q, const void* k, const void* v,
+                             void* out, float* lse, const Workspace& ws, bool rectify,
+                             bool text, cudaStream_t st, int* launches);
+bool tc_supported(const Geometry& g);
+cudaError_t launch_attn_tc(const Geometry& g, const void* q, const void* k, const void* v,
+                           void* out, float* lse, const Workspace& ws, bool rectify,
+                           bool text, cudaStream_t st, int* launches);
+
+}  // namespace rsa

@@ -1,0 +1,449 @@
+// K2: pooled scoring, IPAR, deterministic block selection, GAPR gate,
+// rectification factors, compensation rows and the kv-block lists K3 walks.
+//
+// Reference (pkg/src/rectattn):
+//   mixed_pooled_scores  ipar.py:36-42     scores = q_pool k_mix^T / sqrt(d), softmax
+//   reallocate           ipar.py:45-66     D = B*sum(A_v) + sum(A_t)
+//   implicit_full_attn   ipar.py:69-86     text re-aggregation -> a_pool (N x M)
+//   build_sparse_mask    masks.py:83-117   stable argsort(-a), sequential cumsum,
+//                                          count = clip(max(ceil(fM), first_p), 1, M)
+//   pooled_scores        masks.py:120-127  video columns == mixed video columns
+//   attention_gain       masks.py:138-146  |B * len_m * s_pool|
+//   pooling_error        masks.py:149-176  closed form from the K1 deficits
+//   compensation_mask    masks.py:179-186  gain > error (ties -> False)
+//   rectification_factors rectify.py:56-63 R = 1 - excluded mass
+//   apply_rectification  rectify.py:84-87  (a_pool masked to applied) @ v_pool
+//
+// Everything is fp64 (the bit-exact mask needs it).  The
+// two GEMM-shaped stages (N x n_cols x d scores, N x d x M compensation) run a
+// register-tiled fp64 GEMM; the per-row stage (softmax, reallocation, sort,
+// cumsum, gate, lists) runs one CTA per query block with a shared-memory
+// bitonic sort on the composite key (weight desc, block index asc) -- exactly
+// numpy's stable argsort of -a_pool.
+#include "rsa_internal.cuh"
+
+#include <cfloat>
+
+namespace rsa {
+namespace {
+
+// ----------------------------------------------------------------------------
+// fp64 GEMM: C[h][r][c] = scale_div( sum_k A[h][r][k] * B'[h][k][c] )
+//   NT (scores):       A = q_pool [N][d], B = k_cat [n_cols][d]
+//   NN (compensation): A = a_pool masked by the applied bit [N][M], B = v_pool [M][d]
+// 64x64 tile, BK = 16, 256 threads x (4x4) outputs; k accumulated in order.
+// ----------------------------------------------------------------------------
+constexpr int GT = 64, GK = 16;
+
+template <bool NT>
+__global__ void __launch_bounds__(256)
+dgemm_kernel(const double* __restrict__ A, const double* __restrict__ Bm,
+             const uint8_t* __restrict__ abits, double* __restrict__ C,
+             int64_t rows, int64_t cols, int64_t K,
+             int64_t a_hstride, int64_t b_hstride, int64_t c_hstride, double divisor) {
+  __shared__ double As[GK][GT + 1];
+  __shared__ double Bs[GK][GT + 1];
+  const int64_t h = blockIdx.z;
+  const int64_t r0 = (int64_t)blockIdx.y * GT, c0 = (int64_t)blockIdx.x * GT;
+  const double* Ah = A + h * a_hstride;
+  const double* Bh = Bm + h * b_hstride;
+  const uint8_t* bits = abits ? abits + h * a_hstride : nullptr;
+  const int tid = threadIdx.x;
+  const int tr = tid / 16, tc = tid % 16;
+  double acc[4][4] = {};
+  for (int64_t k0 = 0; k0 < K; k0 += GK) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int e = tid + i * 256;       // 0..1023
+      const int rr = e / GK, kk = e % GK;
+      const int64_t gr = r0 + rr, gk = k0 + kk;
+      double a = 0.0;
+      if (gr < rows && gk < K) {
+        a = Ah[gr * K + gk];
+        if (bits && !(bits[gr * K + gk] & BIT_APPLIED)) a = 0.0;
+      }
+      As[kk][rr] = a;
+      double b = 0.0;
+      if (NT) {
+        const int64_t gc = c0 + rr;
+        if (gc < cols && gk < K) b = Bh[gc * K + gk];
+        Bs[kk][rr] = b;
+      } else {
+        const int cc = e % GT, kb = e / GT;
+        const int64_t gc = c0 + cc, gkb = k0 + kb;
+        if (gc < cols && gkb < K) b = Bh[gkb * cols + gc];
+        Bs[kb][cc] = b;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < GK; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { a[i] = As[kk][tr + 16 * i]; b[i] = Bs[kk][tc + 16 * i]; }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  double* Ch = C + h * c_hstride;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t gr = r0 + tr + 16 * i, gc = c0 + tc + 16 * j;
+      if (gr < rows && gc < cols) Ch[gr * cols + gc] = divisor == 1.0 ? acc[i][j] : acc[i][j] / divisor;
+    }
+}
+
+// ----------------------------------------------------------------------------
+// block-wide deterministic reductions (fixed tree order)
+// ----------------------------------------------------------------------------
+constexpr int RT = 256;
+
+__device__ __forceinline__ double warp_sum(double x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+__device__ __forceinline__ double warp_max(double x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+  return x;
+}
+__device__ double block_sum(double x, double* red) {
+  x = warp_sum(x);
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+  __syncthreads();
+  if (l == 0) red[w] = x;
+  __syncthreads();
+  double y = (threadIdx.x < RT / 32) ? red[threadIdx.x] : 0.0;
+  if (w == 0) y = warp_sum(y);
+  if (threadIdx.x == 0) red[0] = y;
+  __syncthreads();
+  return red[0];
+}
+__device__ double block_max(double x, double* red) {
+  x = warp_max(x);
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+  __syncthreads();
+  if (l == 0) red[w] = x;
+  __syncthreads();
+  double y = (threadIdx.x < RT / 32) ? red[threadIdx.x] : -DBL_MAX;
+  if (w == 0) y = warp_max(y);
+  if (threadIdx.x == 0) red[0] = y;
+  __syncthreads();
+  return red[0];
+}
+__device__ int block_excl_scan(int x, int* tmp, int* total) {
+  // Hillis-Steele over 256 threads (deterministic, integer)
+  tmp[threadIdx.x] = x;
+  __syncthreads();
+  for (int o = 1; o < RT; o <<= 1) {
+    int y = threadIdx.x >= o ? tmp[threadIdx.x - o] : 0;
+    __syncthreads();
+    tmp[threadIdx.x] += y;
+    __syncthreads();
+  }
+  const int incl = tmp[threadIdx.x];
+  *total = tmp[RT - 1];
+  __syncthreads();
+  return incl - x;
+}
+
+struct SelectParams {
+  Geometry g;
+  Workspace ws;
+  double p;
+  int64_t k_floor;
+  int radius;
+  int force_text;
+  int variant;
+  double inv_sqrt_d;
+  int p2;  // power of two >= M for the sort
+};
+
+// (value desc, index asc) ordering == numpy argsort(-a, kind="stable")
+__device__ __forceinline__ bool before(double va, int ia, double vb, int ib) {
+  return va > vb || (va == vb && ia < ib);
+}
+
+__global__ void __launch_bounds__(RT) select_rows_kernel(SelectParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const Geometry& g = P.g;
+  const Workspace& ws = P.ws;
+  const int64_t n = blockIdx.x, h = blockIdx.y;
+  const int64_t N = g.N, M = g.M, Tt = g.Tt, n_cols = g.n_cols;
+  const int64_t n_mix = N + Tt;
+  double* sa = reinterpret_cast<double*>(smem_raw);     // [n_mix] a_mix / a_hat
+  double* ap = sa + n_mix;                               // [M] a_pool row
+  double* sv = ap + M;                                   // [p2] sort values
+  int* si = reinterpret_cast<int*>(sv + P.p2);           // [p2] sort indices
+  uint8_t* bits = reinterpret_cast<uint8_t*>(si + P.p2); // [M]
+  __shared__ double red[RT / 32];
+  __shared__ int scan_tmp[RT];
+  __shared__ int sh_count;
+
+  const double* srow = ws.scores + (h * N + n) * n_cols;
+
+  // ---- IPAR: softmax over the mixed row (core.py:204-208) ----
+  double mx = -DBL_MAX;
+  for (int64_t j = threadIdx.x; j < n_mix; j += RT) { const double s = srow[j]; sa[j] = s; mx = fmax(mx, s); }
+  mx = block_max(mx, red);
+  double part = 0.0;
+  for (int64_t j = threadIdx.x; j < n_mix; j += RT) { const double e = exp(sa[j] - mx); sa[j] = e; part += e; }
+  const double tot = block_sum(part, red);
+  for (int64_t j = threadIdx.x; j < n_mix; j += RT) sa[j] = sa[j] / tot;
+  __syncthreads();
+
+  // ---- reallocation (ipar.py:45-66) ----
+  if (Tt > 0 && g.B > 1) {
+    double pv = 0.0, pt = 0.0;
+    for (int64_t j = threadIdx.x; j < n_mix; j += RT) { if (j < N) pv += sa[j]; else pt += sa[j]; }
+    const double sum_v = block_sum(pv, red);
+    const double sum_t = block_sum(pt, red);
+    const double D = (double)g.B * sum_v + sum_t;
+    if (D <= 0.0) { if (threadIdx.x == 0) atomicOr(ws.status + ST_DEGENERATE, 1); }
+    for (int64_t j = threadIdx.x; j < n_mix; j += RT)
+      sa[j] = (j < N) ? ((double)g.B * sa[j]) / D : sa[j] / D;
+    __syncthreads();
+  }
+  // ---- a_pool row: video part + text re-aggregation (ipar.py:76-83) ----
+  for (int64_t m = threadIdx.x; m < N; m += RT) ap[m] = sa[m];
+  for (int64_t j = 0; j < g.n_text; ++j) {
+    const int64_t lo = N + j * g.B, hi = min(N + (j + 1) * g.B, n_mix);
+    double pj = 0.0;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += RT) pj += sa[i];
+    const double sj = block_sum(pj, red);
+    if (threadIdx.x == 0) ap[N + j] = sj;
+  }
+  __syncthreads();
+  double* ap_out = ws.a_pool + (h * N + n) * M;
+  for (int64_t m = threadIdx.x; m < M; m += RT) { ap_out[m] = ap[m]; bits[m] = 0; }
+  __syncthreads();
+
+  // ---- selection (masks.py:83-117) ----
+  const bool full = P.variant == RSA_VARIANT_FULL;
+  if (full) {
+    for (int64_t m = threadIdx.x; m < M; m += RT) bits[m] = BIT_MASK | BIT_IMPORTANCE;
+  } else {
+    for (int i = threadIdx.x; i < P.p2; i += RT) {
+      sv[i] = i < M ? ap[i] : -1.0;
+      si[i] = i < M ? i : 0x7fffffff;
+    }
+    __syncthreads();
+    for (int kk = 2; kk <= P.p2; kk <<= 1) {
+      for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+        for (int i = threadIdx.x; i < P.p2; i += RT) {
+          const int ixj = i ^ jj;
+          if (ixj > i) {
+            const bool up = (i & kk) == 0;
+            const double va = sv[i], vb = sv[ixj];
+            const int ia = si[i], ib = si[ixj];
+            const bool swap = up ? before(vb, ib, va, ia) : before(va, ia, vb, ib);
+            if (swap) { sv[i] = vb; sv[ixj] = va; si[i] = ib; si[ixj] = ia; }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    if (threadIdx.x == 0) {
+      // sequential cumsum in sorted order, exactly as numpy.cumsum (masks.py:99-102)
+      int64_t first_p = M;
+      double cum = 0.0;
+      for (int64_t i = 0; i < M; ++i) {
+        cum += sv[i];
+        if (cum >= P.p) { first_p = i + 1; break; }
+      }
+      int64_t count = first_p > P.k_floor ? first_p : P.k_floor;
+      count = count < 1 ? 1 : (count > M ? M : count);
+      sh_count = (int)count;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < sh_count; i += RT) bits[si[i]] = BIT_IMPORTANCE;
+    __syncthreads();
+    for (int64_t m = threadIdx.x; m < M; m += RT) {
+      uint8_t b = bits[m];
+      const int64_t dist = m > n ? m - n : n - m;
+      if (dist <= P.radius) b |= BIT_ADJ;
+      if ((b & (BIT_IMPORTANCE | BIT_ADJ)) || (P.force_text && M > N && m >= N)) b |= BIT_MASK;
+      bits[m] = b;
+    }
+  }
+  __syncthreads();
+
+  // ---- R = 1 - excluded mass (rectify.py:56-63) ----
+  double ex = 0.0;
+  for (int64_t m = threadIdx.x; m < M; m += RT) ex += (bits[m] & BIT_MASK) ? 0.0 : ap[m];
+  const double R = 1.0 - block_sum(ex, red);
+
+  // ---- GAPR gate: gain vs first-order error (masks.py:138-186) ----
+  const bool deficit = ws.status[ST_DEFICIT] != 0;
+  const int64_t d = g.d;
+  for (int64_t m = threadIdx.x; m < M; m += RT) {
+    const double len = (m < N) ? (double)g.B : (m == M - 1 ? (double)g.last_len : (double)g.B);
+    const double s = (m < N) ? srow[m] : srow[N + Tt + (m - N)];
+    const double gain = fabs(((double)g.B * len) * s);
+    double err = 0.0;
+    if (deficit) {
+      const int64_t krow = (m < N) ? m : N + Tt + (m - N);
+      const double* kp = ws.k_cat + (h * n_cols + krow) * d;
+      const double* kd = ws.k_def + (h * M + m) * d;
+      const double* qp = ws.q_pool + (h * N + n) * d;
+      const double* qd = ws.q_def + (h * N + n) * d;
+      double d1 = 0.0, d2 = 0.0;
+      for (int64_t c = 0; c < d; ++c) { d1 = fma(qd[c], kp[c], d1); d2 = fma(qp[c], kd[c], d2); }
+      const double t1 = (d1 * len) * P.inv_sqrt_d;
+      const double t2 = ((double)g.B * d2) * P.inv_sqrt_d;
+      err = fabs(t1 + t2);
+    }
+    uint8_t b = bits[m];
+    if (gain > err) b |= BIT_COMP;
+    const bool masked = b & BIT_MASK;
+    bool applied = false;
+    if (P.variant == RSA_VARIANT_SPARSE_RECTIFIED) applied = !masked && (b & BIT_COMP);
+    else if (P.variant == RSA_VARIANT_COMPENSATE_ALL) applied = !masked;
+    if (applied) b |= BIT_APPLIED;
+    bits[m] = b;
+  }
+  __syncthreads();
+  uint8_t* bits_out = ws.mask_bits + (h * N + n) * M;
+  for (int64_t m = threadIdx.x; m < M; m += RT) bits_out[m] = bits[m];
+  if (threadIdx.x == 0) {
+    ws.r[h * N + n] = R;
+    const bool rect = P.variant == RSA_VARIANT_SPARSE_RECTIFIED ||
+                      P.variant == RSA_VARIANT_SPARSE_RECTIFIED_NO_GAPR ||
+                      P.variant == RSA_VARIANT_COMPENSATE_ALL;
+    ws.r_eff[h * N + n] = rect ? (float)R : 1.0f;
+  }
+
+  // ---- ascending kv list (kernel.py:92 np.flatnonzero) ----
+  const int64_t chunk = (M + RT - 1) / RT;
+  const int64_t lo = threadIdx.x * chunk, hi = min(lo + chunk, M);
+  int local = 0;
+  for (int64_t m = lo; m < hi; ++m) local += (bits[m] & BIT_MASK) ? 1 : 0;
+  int total;
+  int off = block_excl_scan(local, scan_tmp, &total);
+  int32_t* list = ws.kv_list + (h * N + n) * M;
+  for (int64_t m = lo; m < hi; ++m)
+    if (bits[m] & BIT_MASK) list[off++] = (int32_t)m;
+  if (threadIdx.x == 0) {
+    ws.kv_count[h * N + n] = total;
+    if (total == 0) atomicOr(ws.status + ST_EMPTY_ROW, 1);
+  }
+}
+
+// kv lists from an explicit caller mask (kernel-only seam)
+__global__ void __launch_bounds__(RT) lists_from_mask_kernel(const uint8_t* __restrict__ mask,
+                                                             Workspace ws, Geometry g) {
+  __shared__ int scan_tmp[RT];
+  const int64_t n = blockIdx.x, h = blockIdx.y, M = g.M;
+  const uint8_t* row = mask + (h * g.N + n) * M;
+  uint8_t* bits_out = ws.mask_bits + (h * g.N + n) * M;
+  const int64_t chunk = (M + RT - 1) / RT;
+  const int64_t lo = threadIdx.x * chunk, hi = min(lo + chunk, M);
+  int local = 0;
+  for (int64_t m = lo; m < hi; ++m) {
+    const bool on = row[m] != 0;
+    bits_out[m] = on ? BIT_MASK : 0;
+    local += on;
+  }
+  int total;
+  int off = block_excl_scan(local, scan_tmp, &total);
+  int32_t* list = ws.kv_list + (h * g.N + n) * M;
+  for (int64_t m = lo; m < hi; ++m)
+    if (row[m]) list[off++] = (int32_t)m;
+  if (threadIdx.x == 0) {
+    ws.kv_count[h * g.N + n] = total;
+    ws.r_eff[h * g.N + n] = 1.0f;
+    if (total == 0) atomicOr(ws.status + ST_EMPTY_ROW, 1);
+  }
+}
+
+// Per 128-row tcgen05 tile: union of the G = 128/B member query blocks' kv
+// lists, ascending, each entry (kv id | member-bit mask << 24).  One warp per tile.
+__global__ void tile_lists_kernel(Workspace ws, Geometry g) {
+  const int G = (int)(kTcTileRows / g.B);
+  const int64_t tiles_per_head = (g.N + G - 1) / G;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  if (warp >= tiles_per_head * g.H) return;
+  const int64_t h = warp / tiles_per_head, t = warp % tiles_per_head;
+  const int gcount = (int)min((int64_t)G, g.N - t * G);
+  const uint8_t* rows = ws.mask_bits + (h * g.N + t * G) * g.M;
+  int32_t* out = ws.tile_list + (h * tiles_per_head + t) * g.M;
+  int count = 0;
+  for (int64_t m0 = 0; m0 < g.M; m0 += 32) {
+    const int64_t m = m0 + lane;
+    uint32_t member = 0;
+    if (m < g.M)
+      for (int gg = 0; gg < gcount; ++gg) member |= (rows[gg * g.M + m] & BIT_MASK) ? (1u << gg) : 0u;
+    const uint32_t ballot = __ballot_sync(0xffffffffu, member != 0);
+    if (member) out[count + __popc(ballot & ((1u << lane) - 1))] = (int32_t)(m | (member << 24));
+    count += __popc(ballot);
+  }
+  if (lane == 0) ws.tile_count[h * tiles_per_head + t] = count;
+}
+
+}  // namespace
+
+cudaError_t launch_select(const Geometry& g, const rsa_config& cfg, int64_t k_floor,
+                          const Workspace& ws, cudaStream_t st, int* launches) {
+  const double sqrt_d = sqrt((double)g.d);
+  // scores = (q_pool @ k_cat^T) / sqrt(d)   (ipar.py:41, masks.py:127)
+  {
+    dim3 grid((unsigned)((g.n_cols + GT - 1) / GT), (unsigned)((g.N + GT - 1) / GT), (unsigned)g.H);
+    dgemm_kernel<true><<<grid, 256, 0, st>>>(ws.q_pool, ws.k_cat, nullptr, ws.scores, g.N,
+                                             g.n_cols, g.d, g.N * g.d, g.n_cols * g.d,
+                                             g.N * g.n_cols, sqrt_d);
+    ++*launches;
+  }
+  SelectParams P;
+  P.g = g;
+  P.ws = ws;
+  P.p = cfg.weight_threshold;
+  P.k_floor = k_floor;
+  P.radius = cfg.adjacency_radius;
+  P.force_text = cfg.force_text_blocks;
+  P.variant = cfg.variant;
+  P.inv_sqrt_d = 1.0 / sqrt_d;
+  int p2 = 1;
+  while (p2 < g.M) p2 <<= 1;
+  P.p2 = p2;
+  const size_t smem = (size_t)(g.N + g.Tt) * 8 + (size_t)g.M * 8 + (size_t)p2 * 12 + (size_t)g.M + 16;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(select_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  select_rows_kernel<<<dim3((unsigned)g.N, (unsigned)g.H), RT, smem, st>>>(P);
+  ++*launches;
+  // compensation rows: (a_pool masked to applied) @ v_pool   (rectify.py:84-87)
+  {
+    dim3 grid((unsigned)((g.d + GT - 1) / GT), (unsigned)((g.N + GT - 1) / GT), (unsigned)g.H);
+    dgemm_kernel<false><<<grid, 256, 0, st>>>(ws.a_pool, ws.v_pool, ws.mask_bits, ws.comp, g.N,
+                                              g.d, g.M, g.N * g.M, g.M * g.d, g.N * g.d, 1.0);
+    ++*launches;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lists_from_mask(const Geometry& g, const uint8_t* mask, const Workspace& ws,
+                                   cudaStream_t st, int* launches) {
+  lists_from_mask_kernel<<<dim3((unsigned)g.N, (unsigned)g.H), RT, 0, st>>>(mask, ws, g);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tile_lists(const Geometry& g, const Workspace& ws, cudaStream_t st,
+                              int* launches) {
+  const int64_t G = kTcTileRows / g.B;
+  const int64_t tiles = g.H * ((g.N + G - 1) / G);
+  const int64_t threads = tiles * 32;
+  tile_lists_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(ws, g);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+}  // namespace rsa

@@ -1,0 +1,32 @@
+"""torch.library registration of the hot path as ``torch.ops.rsa_b200.*``.
+
+The ops call straight into the C ABI (include/rsa_b200.h) on the current
+stream; fake (meta) kernels describe output shapes so the op composes with
+tracing.  A model integration replaces its attention call with
+``torch.ops.rsa_b200.rectified_sparse_attention(q, k, v, num_text, block, ...)``.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from .pipeline import rectified_sparse_attention as _impl
+
+_LIB_NS = "rsa_b200"
+
+
+@torch.library.custom_op(f"{_LIB_NS}::rectified_sparse_attention", mutates_args=())
+def rectified_sparse_attention_op(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
+                                  num_text_tokens: int, block: int, top_k_fraction: float,
+                                  weight_threshold: float, adjacency_radius: int,
+                                  force_text_blocks: bool, variant: str) -> torch.Tensor:
+    return _impl(q, k, v, num_text_tokens=num_text_tokens, block=block,
+                 top_k_fraction=top_k_fraction, weight_threshold=weight_threshold,
+                 adjacency_radius=adjacency_radius, force_text_blocks=force_text_blocks,
+                 variant=variant)
+
+
+@rectified_sparse_attention_op.register_fake
+def _(q, k, v, num_text_tokens, block, top_k_fraction, weight_threshold, adjacency_radius,
+      force_text_blocks, variant):
+    return torch.empty_like(q)

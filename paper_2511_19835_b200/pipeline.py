@@ -1,0 +1,268 @@
+"""The drop-in entry points: the reference's pipeline / kernel API backed by
+librsa_b200.so, plus the batched tensor op a model integration calls.
+
+Reference entry points mirrored here (pkg/src/rectattn):
+  rectified_attention_pipeline(problem, config, variant)   rectify.py:107-176
+  block_sparse_attention(q_v, k, v, mask, grid, counters)  kernel.py:65-117
+  text_full_attention(q_t, k, v, block)                    kernel.py:120-145
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .core import (VARIANTS, AttentionOutput, AttentionProblem, BlockGrid, CompensationMask,
+                   ImplicitAttention, PipelineAccounting, PipelineResult, PooledSet,
+                   RectificationFactors, SparseMask, SparsityConfig, _is_torch, check_matrix,
+                   partition, stage_op_counts)
+from .errors import ConfigError, EmptyRowError, NativeError, ShapeError
+
+MASK_BIT, IMPORTANCE_BIT, COMP_BIT, ADJ_BIT, APPLIED_BIT = 1, 2, 4, 8, 16
+
+
+def _device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise NativeError("no CUDA device: the B200 kernels are the only implementation "
+                          "(there is no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _as_tensor(x, device) -> torch.Tensor:
+    if _is_torch(x):
+        return x.to(device)
+    return torch.from_numpy(np.ascontiguousarray(x)).to(device)
+
+
+def _ptr(t: torch.Tensor | None):
+    return C.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def workspace_for(shape: nat.Shape, device) -> torch.Tensor:
+    size = nat.lib().rsa_workspace_size(C.byref(shape))
+    if size == 0:
+        nat.check(nat.lib().rsa_plan(C.byref(shape), None, None))
+    return torch.empty(size, dtype=torch.uint8, device=device)
+
+
+def _view(ws: torch.Tensor, offset: int, dtype, shape) -> torch.Tensor:
+    n = int(np.prod(shape))
+    itemsize = torch.empty((), dtype=dtype).element_size()
+    return ws[offset:offset + n * itemsize].view(dtype).view(*shape)
+
+
+def _cfg_tuple(config) -> tuple:
+    return (config.top_k_fraction, config.weight_threshold, config.adjacency_radius,
+            config.force_text_blocks)
+
+
+# ---------------------------------------------------------------------------
+# rectify.py:107-176
+# ---------------------------------------------------------------------------
+
+def rectified_attention_pipeline(problem: AttentionProblem, config: SparsityConfig,
+                                 variant: str = "sparse-rectified", *, kernel: str = "auto",
+                                 timing: bool = False) -> PipelineResult:
+    """Pool, implicit full attention, gain/error and compensation mask, sparse
+    mask, sparse kernel plus text full attention, then the variant's
+    rectification step -- all on the GPU (K1 -> K2 -> K3+K4)."""
+    if variant not in VARIANTS:
+        raise ConfigError(f"unknown variant {variant!r}, expected one of {VARIANTS}")
+    dev = _device()
+    host = not _is_torch(problem.q_video)
+    grid = partition(problem)
+    t_v, t_t, d = problem.t_v, problem.t_t, problem.d
+    q = torch.cat([_as_tensor(problem.q_video, dev), _as_tensor(problem.q_text, dev)]).contiguous()
+    k = _as_tensor(problem.k, dev).contiguous()
+    v = _as_tensor(problem.v, dev).contiguous()
+    dtype = str(q.dtype).replace("torch.", "")
+    shape = nat.make_shape(1, t_v, t_t, d, problem.block, dtype, kernel)
+    cfg = nat.make_config(*_cfg_tuple(config), variant)
+    nat.plan(shape, cfg)
+    ws = workspace_for(shape, dev)
+    out = torch.empty_like(q)
+    lse = torch.empty(q.shape[0], dtype=torch.float32, device=dev)
+    lib, st = nat.lib(), _stream()
+    acct = PipelineAccounting()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if timing else None
+    if ev:
+        ev[0].record()
+    nat.check(lib.rsa_pool(C.byref(shape), _ptr(q), _ptr(k), _ptr(v), _ptr(ws), st))
+    if ev:
+        ev[1].record()
+    nat.check(lib.rsa_select(C.byref(shape), C.byref(cfg), _ptr(ws), st))
+    if ev:
+        ev[2].record()
+    nat.check(lib.rsa_attention(C.byref(shape), C.byref(cfg), _ptr(q), _ptr(k), _ptr(v),
+                                _ptr(out), _ptr(lse), _ptr(ws), st))
+    if ev:
+        ev[3].record()
+    nat.check(lib.rsa_check_device_status(_ptr(ws), st))  # synchronises (reference raises eagerly)
+    if ev:
+        acct.stage_wall_ms = {"pool": ev[0].elapsed_time(ev[1]),
+                              "select": ev[1].elapsed_time(ev[2]),
+                              "attention": ev[2].elapsed_time(ev[3])}
+    return _result(problem, grid, shape, ws, out, lse, variant, acct, host)
+
+
+def _result(problem, grid: BlockGrid, shape, ws, out, lse, variant, acct, host) -> PipelineResult:
+    L = nat.layout(shape)
+    N, M, d, t_v, t_t = grid.n_q, grid.n_kv, problem.d, problem.t_v, problem.t_t
+    n_cols = N + t_t + (M - N)
+    f64 = torch.float64
+    q_pool = _view(ws, L["q_pool"], f64, (N, d))
+    k_cat = _view(ws, L["k_cat"], f64, (n_cols, d))
+    v_pool = _view(ws, L["v_pool"], f64, (M, d))
+    scores = _view(ws, L["scores"], f64, (N, n_cols))
+    a_pool = _view(ws, L["a_pool"], f64, (N, M))
+    bits = _view(ws, L["mask_bits"], torch.uint8, (N, M))
+    r = _view(ws, L["r"], f64, (N,))
+    mask = (bits & MASK_BIT) != 0
+    conv = (lambda x: x.detach().cpu().numpy()) if host else (lambda x: x.clone())
+    lens = torch.tensor(grid.kv_block_lengths(), dtype=torch.int64, device=bits.device)
+    acct.kernel_inner_product_ops = int((mask.to(torch.int64) * lens[None, :]).sum().item()) * grid.block * d
+    acct.stage_ops = stage_op_counts(grid, d)
+    out_dtype = problem.q_video.dtype
+    o = conv(out)
+    o_video, o_text = o[:t_v], o[t_v:]
+    if host:
+        o_video, o_text = o_video.astype(out_dtype), o_text.astype(out_dtype)
+    return PipelineResult(
+        output=AttentionOutput(o_video=o_video, o_text=o_text,
+                               row_log_denominators=conv(lse[:t_v].to(f64))),
+        factors=RectificationFactors(r=conv(r)),
+        implicit=ImplicitAttention(conv(a_pool), scores[:, :N + t_t].clone(), N, grid.block, t_t, conv),
+        sparse_mask=SparseMask(mask=conv(mask), importance=conv((bits & IMPORTANCE_BIT) != 0),
+                               adjacency=conv((bits & ADJ_BIT) != 0),
+                               retained_count=conv(mask.sum(dim=1))),
+        comp_mask=CompensationMask(mask=conv((bits & COMP_BIT) != 0)),
+        accounting=acct, grid=grid,
+        pooled=PooledSet(q_pool=conv(q_pool), k_v_pool=conv(k_cat[:N]), v_pool=conv(v_pool),
+                         k_mix_pool=conv(k_cat[:N + t_t])),
+        variant=variant)
+
+
+# ---------------------------------------------------------------------------
+# kernel.py:65-117 and kernel.py:120-145
+# ---------------------------------------------------------------------------
+
+def block_sparse_attention(q_v, k, v, mask, grid: BlockGrid, counters: dict | None = None,
+                           *, kernel: str = "auto"):
+    """Sparse attention of the video queries over an explicit (N, M) block mask.
+    Returns ``(o_video, row_log_denominators)``."""
+    check_matrix(q_v, "q_v")
+    check_matrix(k, "k")
+    check_matrix(v, "v")
+    block_mask = getattr(mask, "mask", mask)
+    host = not _is_torch(q_v)
+    dev = _device()
+    bm = _as_tensor(np.asarray(block_mask, dtype=bool) if not _is_torch(block_mask) else block_mask,
+                    dev).to(torch.bool)
+    if tuple(bm.shape) != (grid.n_q, grid.n_kv):
+        raise ShapeError(f"mask shape {tuple(bm.shape)} != (N, M) = {(grid.n_q, grid.n_kv)}")
+    if q_v.shape[0] != grid.n_q * grid.block:
+        raise ShapeError(f"q_v has {q_v.shape[0]} rows, expected N*B = {grid.n_q * grid.block}")
+    if tuple(k.shape) != tuple(v.shape):
+        raise ShapeError(f"k shape {tuple(k.shape)} != v shape {tuple(v.shape)}")
+    empty = ~bm.any(dim=1)
+    if bool(empty.any()):
+        raise EmptyRowError(f"mask rows {torch.nonzero(empty).flatten().tolist()} retain no key block")
+    t_v, d = q_v.shape[0], q_v.shape[1]
+    t_t = k.shape[0] - t_v
+    qv = _as_tensor(q_v, dev)
+    q = torch.cat([qv, torch.zeros(t_t, d, dtype=qv.dtype, device=dev)]).contiguous()
+    kk = _as_tensor(k, dev).contiguous()
+    vv = _as_tensor(v, dev).contiguous()
+    shape = nat.make_shape(1, t_v, t_t, d, grid.block, str(q.dtype).replace("torch.", ""), kernel)
+    ws = workspace_for(shape, dev)
+    out = torch.zeros_like(q)
+    lse = torch.empty(q.shape[0], dtype=torch.float32, device=dev)
+    m8 = bm.to(torch.uint8).contiguous()
+    nat.check(nat.lib().rsa_block_sparse_attention(C.byref(shape), _ptr(q), _ptr(kk), _ptr(vv),
+                                                   _ptr(m8), _ptr(out), _ptr(lse), _ptr(ws), _stream()))
+    nat.check(nat.lib().rsa_check_device_status(_ptr(ws), _stream()))
+    if counters is not None:
+        lens = torch.tensor(grid.kv_block_lengths(), dtype=torch.int64, device=dev)
+        ops = int((bm.to(torch.int64) * lens[None, :]).sum().item()) * grid.block * d
+        counters["inner_product_ops"] = counters.get("inner_product_ops", 0) + ops
+    o_video, ld = out[:t_v], lse[:t_v].to(torch.float64)
+    if host:
+        return o_video.cpu().numpy().astype(q_v.dtype), ld.cpu().numpy()
+    return o_video, ld
+
+
+def text_full_attention(q_t, k, v, block: int = 128):
+    """Full attention for text queries over every key, tiled by ``block``."""
+    check_matrix(q_t, "q_t")
+    check_matrix(k, "k")
+    check_matrix(v, "v")
+    if q_t.shape[1] != k.shape[1]:
+        raise ShapeError(f"q_t width {q_t.shape[1]} != k width {k.shape[1]}")
+    if tuple(k.shape) != tuple(v.shape):
+        raise ShapeError(f"k shape {tuple(k.shape)} != v shape {tuple(v.shape)}")
+    host = not _is_torch(q_t)
+    if q_t.shape[0] == 0:
+        return (np.empty((0, v.shape[1]), dtype=q_t.dtype) if host
+                else torch.empty(0, v.shape[1], dtype=q_t.dtype, device=q_t.device))
+    dev = _device()
+    q = _as_tensor(q_t, dev).contiguous()
+    kk = _as_tensor(k, dev).contiguous()
+    vv = _as_tensor(v, dev).contiguous()
+    out = torch.empty_like(q)
+    code = nat.DTYPE_CODES[str(q.dtype).replace("torch.", "")]
+    nat.check(nat.lib().rsa_text_full_attention(1, q.shape[0], kk.shape[0], q.shape[1], int(block),
+                                                code, _ptr(q), _ptr(kk), _ptr(vv), _ptr(out), None,
+                                                None, _stream()))
+    if host:
+        return out.cpu().numpy()
+    return out
+
+
+# ---------------------------------------------------------------------------
+# batched tensor op: [batch, heads, T, d] (video tokens first)
+# ---------------------------------------------------------------------------
+
+def rectified_sparse_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *,
+                               num_text_tokens: int, block: int = 128,
+                               top_k_fraction: float | None = None,
+                               weight_threshold: float = 0.0, adjacency_radius: int = 0,
+                               force_text_blocks: bool = False,
+                               variant: str = "sparse-rectified", sparsity: float | None = None,
+                               kernel: str = "auto", lse: torch.Tensor | None = None,
+                               workspace: torch.Tensor | None = None,
+                               check_status: bool = False) -> torch.Tensor:
+    """Rectified block-sparse attention for every (batch, head) of q/k/v
+    ([..., T, d], the last ``num_text_tokens`` rows text).  ``sparsity=s`` is
+    shorthand for top_k_fraction = 1 - s with p = 0, r = 0, no forced text.
+    Stream-ordered; no host synchronisation unless ``check_status``."""
+    if sparsity is not None:
+        top_k_fraction, weight_threshold, adjacency_radius, force_text_blocks = 1.0 - sparsity, 0.0, 0, False
+    if top_k_fraction is None:
+        top_k_fraction = 0.1
+    if q.dim() < 3 or q.shape != k.shape or k.shape != v.shape:
+        raise ShapeError(f"q/k/v must share a [..., T, d] shape, got {tuple(q.shape)}, "
+                         f"{tuple(k.shape)}, {tuple(v.shape)}")
+    if not q.is_cuda:
+        raise NativeError("rectified_sparse_attention needs CUDA tensors (no CPU fallback)")
+    T, d = q.shape[-2], q.shape[-1]
+    heads = int(np.prod(q.shape[:-2]))
+    t_t = int(num_text_tokens)
+    shape = nat.make_shape(heads, T - t_t, t_t, d, block, str(q.dtype).replace("torch.", ""), kernel)
+    cfg = nat.make_config(top_k_fraction, weight_threshold, adjacency_radius, force_text_blocks, variant)
+    nat.plan(shape, cfg)
+    q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+    if workspace is None:
+        workspace = workspace_for(shape, q.device)
+    out = torch.empty_like(q)
+    nat.check(nat.lib().rsa_forward(C.byref(shape), C.byref(cfg), _ptr(q), _ptr(k), _ptr(v),
+                                    _ptr(out), _ptr(lse), _ptr(workspace), _stream()))
+    if check_status:
+        nat.check(nat.lib().rsa_check_device_status(_ptr(workspace), _stream()))
+    return out

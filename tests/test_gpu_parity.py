@@ -1,0 +1,253 @@
+"""GPU parity: the sm_100a pipeline (through the C ABI) against the CPU oracle
+and the reference goldens.  Bars (BASELINE.json):
+  * block masks / importance / gain>error gate: bit-exact
+  * a_pool, R: <= 1e-12 abs; pooled tensors bit-exact
+  * fp64 inputs: outputs <= 1e-12; fp32 inputs: <= 1e-5 (reference tolerances,
+    pkg/tests/test_kernel.py:62-77)
+  * bf16 inputs (tensor-core path): max-abs <= 2e-2 and cosine >= 0.999 vs the
+    fp32 oracle pipeline on the same bf16-valued inputs.
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import paper_2511_19835_b200 as rsa  # noqa: E402
+from paper_2511_19835_b200 import AttentionProblem, SparsityConfig, partition  # noqa: E402
+from conftest import N_TINY, tiny_case  # noqa: E402
+from oracle import rsa_oracle as O  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+BF16_MAX_ABS = 2e-2
+BF16_MIN_COS = 0.999
+
+
+def to_bf16_tensor(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(torch.bfloat16).cuda()
+
+
+def run_np(qv, qt, k, v, block, f, p, r, force, variant, kernel="auto"):
+    prob = AttentionProblem(q_video=qv, q_text=qt, k=k, v=v, d=qv.shape[1], block=block)
+    return rsa.rectified_attention_pipeline(prob, SparsityConfig(f, p, r, force), variant, kernel=kernel)
+
+
+# ---------------------------------------------------------------- tiny goldens
+
+@pytest.mark.parametrize("i", range(N_TINY))
+def test_tiny_cases_against_reference_goldens(tiny_golden, i):
+    (qv, qt, k, v), m = tiny_case(tiny_golden, i)
+    tol = 1e-12 if qv.dtype == np.float64 else 1e-5
+    for variant in O.VARIANTS:
+        res = run_np(qv, qt, k, v, m["block"], m["f"], m["p"], m["r"], m["force"], variant)
+        tag = f"c{i}_{variant}"
+        assert res.output.o_video.dtype == qv.dtype
+        np.testing.assert_allclose(res.output.o_video, tiny_golden[f"{tag}_o_video"], atol=tol, rtol=0)
+        np.testing.assert_allclose(res.output.o_text, tiny_golden[f"{tag}_o_text"], atol=tol, rtol=0)
+        if variant == "sparse-rectified":
+            np.testing.assert_array_equal(res.sparse_mask.mask, tiny_golden[f"c{i}_mask"])
+            np.testing.assert_array_equal(res.sparse_mask.importance, tiny_golden[f"c{i}_importance"])
+            np.testing.assert_array_equal(res.comp_mask.mask, tiny_golden[f"c{i}_comp"])
+            np.testing.assert_allclose(res.factors.r, tiny_golden[f"c{i}_r"], atol=1e-12, rtol=0)
+            np.testing.assert_allclose(res.implicit.a_pool, tiny_golden[f"c{i}_a_pool"], atol=1e-12, rtol=0)
+            np.testing.assert_array_equal(res.pooled.q_pool, tiny_golden[f"c{i}_q_pool"])
+            np.testing.assert_array_equal(res.pooled.v_pool, tiny_golden[f"c{i}_v_pool"])
+            np.testing.assert_array_equal(res.pooled.k_mix_pool, tiny_golden[f"c{i}_k_mix"])
+            assert rsa.check_result_invariants(res)
+
+
+# ---------------------------------------------------------------- cfg1 (bf16)
+
+def cfg1_inputs(seed):
+    qv, qt, k, v = O.gen_synthetic(seed, 3840, 256, 64, 64, (1, 60, 64), 1.0, 2.0, 0.3)
+    return tuple(O.round_to_bf16(x) for x in (qv, qt, k, v))
+
+
+def bf16_problem(qv, qt, k, v, block):
+    return AttentionProblem(q_video=to_bf16_tensor(qv), q_text=to_bf16_tensor(qt),
+                            k=to_bf16_tensor(k), v=to_bf16_tensor(v), d=qv.shape[1], block=block)
+
+
+def assert_bf16_close(got, ref, what):
+    got = got.float().cpu().numpy().astype(np.float64) if torch.is_tensor(got) else np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    err = np.abs(got - ref).max()
+    cos = O.cosine(got, ref)
+    assert err <= BF16_MAX_ABS and cos >= BF16_MIN_COS, f"{what}: max-abs {err:.3e}, cos {cos:.6f}"
+
+
+@pytest.mark.parametrize("seed", [42, 43])
+@pytest.mark.parametrize("kernel", ["auto", "simt"])
+def test_cfg1_bf16_masks_bit_exact_and_outputs(cfg1_golden, seed, kernel):
+    qv, qt, k, v = cfg1_inputs(seed)
+    prob = bf16_problem(qv, qt, k, v, 64)
+    for f in (0.5, 0.25, 0.1, 0.05):
+        for p in (0.0, 0.5):
+            res = rsa.rectified_attention_pipeline(prob, SparsityConfig(f, p, 0, False),
+                                                   "sparse-rectified", kernel=kernel)
+            mask = res.sparse_mask.mask.cpu().numpy()
+            np.testing.assert_array_equal(np.packbits(mask, axis=1), cfg1_golden[f"s{seed}_f{f}_p{p}_mask"])
+            np.testing.assert_allclose(res.factors.r.cpu().numpy(), cfg1_golden[f"s{seed}_f{f}_p{p}_r"],
+                                       atol=1e-12, rtol=0)
+            np.testing.assert_array_equal(np.packbits(res.comp_mask.mask.cpu().numpy(), axis=1),
+                                          cfg1_golden[f"s{seed}_comp"])
+            assert_bf16_close(res.output.o_video[::32], cfg1_golden[f"s{seed}_f{f}_p{p}_sparse-rectified_o_rows"],
+                              f"f={f} p={p} video")
+            assert_bf16_close(res.output.o_text[::8], cfg1_golden[f"s{seed}_f{f}_p{p}_sparse-rectified_ot_rows"],
+                              f"f={f} p={p} text")
+    np.testing.assert_allclose(res.implicit.a_pool.cpu().numpy(), cfg1_golden[f"s{seed}_a_pool"],
+                               atol=1e-12, rtol=0)
+
+
+@pytest.mark.parametrize("variant", O.VARIANTS)
+def test_cfg1_bf16_all_variants_full_output_vs_oracle(variant):
+    qv, qt, k, v = cfg1_inputs(42)
+    res = rsa.rectified_attention_pipeline(bf16_problem(qv, qt, k, v, 64),
+                                           SparsityConfig(0.1, 0.0, 0, False), variant)
+    ref = O.pipeline(qv, qt, k, v, 64, 0.1, 0.0, 0, False, variant)
+    np.testing.assert_array_equal(res.sparse_mask.mask.cpu().numpy(), ref["mask"])
+    assert_bf16_close(res.output.o_video, ref["o_video"], f"{variant} video")
+    assert_bf16_close(res.output.o_text, ref["o_text"], f"{variant} text")
+
+
+def test_batched_tensor_op_matches_per_head_oracle():
+    heads = [cfg1_inputs(s) for s in (42, 43)]
+    q = torch.stack([torch.cat([to_bf16_tensor(h[0]), to_bf16_tensor(h[1])]) for h in heads])[None]
+    k = torch.stack([to_bf16_tensor(h[2]) for h in heads])[None]
+    v = torch.stack([to_bf16_tensor(h[3]) for h in heads])[None]
+    out = rsa.rectified_sparse_attention(q, k, v, num_text_tokens=256, block=64, sparsity=0.9,
+                                         check_status=True)
+    assert out.shape == q.shape and out.dtype == torch.bfloat16
+    for i, (qv, qt, kk, vv) in enumerate(heads):
+        ref = O.pipeline(qv, qt, kk, vv, 64, 1.0 - 0.9, 0.0, 0, False, "sparse-rectified")
+        assert_bf16_close(out[0, i], np.concatenate([ref["o_video"], ref["o_text"]]), f"head {i}")
+
+
+def test_torch_library_op():
+    from paper_2511_19835_b200 import ops  # noqa: F401  (registers torch.ops.rsa_b200)
+    qv, qt, k, v = cfg1_inputs(42)
+    q = torch.cat([to_bf16_tensor(qv), to_bf16_tensor(qt)])[None]
+    out = torch.ops.rsa_b200.rectified_sparse_attention(q, to_bf16_tensor(k)[None], to_bf16_tensor(v)[None],
+                                                        256, 64, 0.1, 0.0, 0, False, "sparse-rectified")
+    ref = O.pipeline(qv, qt, k, v, 64, 0.1, 0.0, 0, False, "sparse-rectified")
+    assert_bf16_close(out[0], np.concatenate([ref["o_video"], ref["o_text"]]), "torch.ops")
+
+
+def test_determinism_bitwise():
+    qv, qt, k, v = cfg1_inputs(43)
+    prob = bf16_problem(qv, qt, k, v, 64)
+    a = rsa.rectified_attention_pipeline(prob, SparsityConfig(0.1, 0.0, 0, False))
+    b = rsa.rectified_attention_pipeline(prob, SparsityConfig(0.1, 0.0, 0, False))
+    assert torch.equal(a.output.o_video, b.output.o_video)
+    assert torch.equal(a.output.o_text, b.output.o_text)
+
+
+# ---------------------------------------------------------------- full-size masks
+
+def test_hunyuan_head_mask_bit_exact(large_golden):
+    """HunyuanVideo 720p head (T_v=118,784, T_t=256, d=128, B=128): the whole
+    pooled path on the GPU reproduces the reference mask bit-for-bit."""
+    qv, qt, k, v = O.gen_synthetic(42, 118784, 256, 128, 128, (29, 64, 64), 1.0, 2.0, 0.3)
+    qv, qt, k, v = (O.round_to_bf16(x) for x in (qv, qt, k, v))
+    prob = bf16_problem(qv, qt, k, v, 128)
+    for f in (0.1, 0.05):
+        res = rsa.rectified_attention_pipeline(prob, SparsityConfig(f, 0.0, 0, False))
+        mask = res.sparse_mask.mask.cpu().numpy()
+        np.testing.assert_array_equal(np.packbits(mask, axis=1), large_golden[f"hv_s42_f{f}_mask"])
+        np.testing.assert_allclose(res.factors.r.cpu().numpy(), large_golden[f"hv_s42_f{f}_r"],
+                                   atol=1e-12, rtol=0)
+        sp = 1.0 - mask.sum() / mask.size
+        assert 0.85 < sp < 0.96
+    # size-independent property at full size: every output row is finite and
+    # R in (0, 1]
+    assert torch.isfinite(res.output.o_video.float()).all()
+    assert (res.factors.r > 0).all() and (res.factors.r <= 1 + 1e-12).all()
+
+
+def test_wan_head_mask_bit_exact(large_golden):
+    rng = np.random.default_rng(42)
+    t = 75520
+    qv = O.round_to_bf16(rng.standard_normal((t, 128)).astype(np.float32))
+    k = O.round_to_bf16(rng.standard_normal((t, 128)).astype(np.float32))
+    v = O.round_to_bf16(rng.standard_normal((t, 128)).astype(np.float32))
+    qt = np.zeros((0, 128), dtype=np.float32)
+    res = rsa.rectified_attention_pipeline(bf16_problem(qv, qt, k, v, 128), SparsityConfig(0.1, 0.0, 0, False))
+    mask = res.sparse_mask.mask.cpu().numpy()
+    np.testing.assert_array_equal(np.packbits(mask, axis=1), large_golden["wan_s42_f0.1_mask"])
+    np.testing.assert_allclose(res.factors.r.cpu().numpy(), large_golden["wan_s42_f0.1_r"], atol=1e-12, rtol=0)
+
+
+# ---------------------------------------------------------------- kernel seams
+
+@pytest.mark.parametrize("precision,tol", [("single", 1e-5), ("double", 1e-12)])
+def test_block_sparse_attention_random_masks(precision, tol):
+    """pkg/tests/test_kernel.py:62-77 on the GPU kernel."""
+    rng = np.random.default_rng(7)
+    dtype = np.float32 if precision == "single" else np.float64
+    for i in range(20):
+        block = int(rng.choice([4, 8, 16]))
+        t_v = block * int(rng.integers(2, 9))
+        t_t = int(rng.integers(0, 9))
+        d = int(rng.choice([8, 16]))
+        qv, qt, k, v = O.random_problem(100 + i, t_v=t_v, t_t=t_t, d=d, dtype=dtype)
+        n, m, last = O.block_geometry(t_v, t_t, block)
+        lens = O.kv_lengths(n, m, block, last)
+        mask = rng.random((n, m)) < 0.4
+        for row in range(n):
+            if not mask[row].any():
+                mask[row, rng.integers(0, m)] = True
+        grid = partition(AttentionProblem(q_video=qv, q_text=qt, k=k, v=v, d=d, block=block))
+        counters = {}
+        out, ld = rsa.block_sparse_attention(qv, k, v, mask, grid, counters=counters)
+        _, expected = O.masked_attention_fp64(qv, k, v, mask, lens, block)
+        assert np.abs(out.astype(np.float64) - expected).max() <= tol
+        assert counters["inner_product_ops"] == int((mask * np.asarray(lens)[None, :]).sum()) * block * d
+        assert ld.shape == (t_v,)
+
+
+def test_block_sparse_attention_empty_row_rejected():
+    qv, qt, k, v = O.random_problem(2, t_v=8, t_t=0, d=8)
+    grid = partition(AttentionProblem(q_video=qv, q_text=qt, k=k, v=v, d=8, block=4))
+    mask = np.zeros((2, 2), dtype=bool)
+    mask[0, 0] = True
+    with pytest.raises(rsa.EmptyRowError):
+        rsa.block_sparse_attention(qv, k, v, mask, grid)
+
+
+@pytest.mark.parametrize("dtype,tol", [(np.float32, 1e-5), (np.float64, 1e-12)])
+def test_text_full_attention(dtype, tol):
+    qv, qt, k, v = O.random_problem(9, t_v=32, t_t=11, d=8, dtype=dtype)
+    out = rsa.text_full_attention(qt, k, v, block=4)
+    _, expected = O.full_attention_fp64(qt, k, v)
+    assert np.abs(out.astype(np.float64) - expected).max() <= tol
+    assert rsa.text_full_attention(qt[:0], k, v, block=4).shape == (0, 8)
+
+
+def test_uniform_rows_tie_break_on_gpu():
+    """Identical keys -> uniform a_pool rows; ties resolve to ascending block
+    index (pkg/tests/test_masks.py:38-49)."""
+    rng = np.random.default_rng(3)
+    d, block, t_v = 8, 4, 32
+    qv = rng.standard_normal((t_v, d))
+    k = np.tile(rng.standard_normal((1, d)), (t_v, 1))
+    v = rng.standard_normal((t_v, d))
+    res = run_np(qv, np.zeros((0, d)), k, v, block, 0.25, 0.0, 1, False, "sparse-rectified")
+    for n in range(8):
+        adj = {m for m in (n - 1, n, n + 1) if 0 <= m < 8}
+        assert set(np.flatnonzero(res.sparse_mask.mask[n])) == adj | {0, 1}
+
+
+def test_zero_sparsity_identity_fp32():
+    """pkg/tests/test_rectify.py:124-129."""
+    qv, qt, k, v = O.random_problem(4, t_v=64, t_t=9, d=16, dtype=np.float32)
+    res = run_np(qv, qt, k, v, 8, 1.0, 0.0, 0, False, "sparse-rectified")
+    _, full = O.full_attention_fp64(np.concatenate([qv, qt]), k, v)
+    got = np.concatenate([res.output.o_video, res.output.o_text]).astype(np.float64)
+    assert np.abs(got - full).max() <= 1e-5
+
+
+def test_errors_map_to_reference_classes():
+    qv, qt, k, v = O.random_problem(0, t_v=8, t_t=0, d=8)
+    with pytest.raises(rsa.ConfigError):
+        run_np(qv, qt, k, v, 4, 0.2, 0.3, 1, True, "bogus")
