@@ -1,0 +1,439 @@
+#!/usr/bin/env python3
+"""Benchmark of the Rectified SpaAttn hot path on B200 (driver contract).
+
+    python bench.py [--gpus N --steps K --warmup W] [--config hv|wan|cfg1] [--impl ours|reference]
+
+One step = one call of the whole hot path (K1 pool -> K2 select -> K3 block-
+sparse attention with the fused IPAR/GAPR epilogue) on the HunyuanVideo 720p
+attention shape (BASELINE.json configs[1]): H=24, T_v=118,784 (928 blocks of
+128; 118,800 rounded down to the reference's T_v mod B == 0 rule), T_t=256,
+d=128, B=128, top_k_fraction 0.1 (90% sparsity), p=0, r=0, no forced text,
+variant sparse-rectified.  Inputs are synthetic bf16 (gen_synthetic-style:
+per-block Gaussian base + 0.3 noise + 3-D positional embedding for video Q/K,
+2x text keys), resident in HBM; they are 2.2 GB, far larger than the 126 MB
+L2, so no flush is needed between steps.
+
+Multi-GPU (torchrun, one rank per GPU): the call's heads are sharded across
+ranks (strong scaling of one fixed call, no collective on the data path);
+ms/call is the max over ranks of the device time.
+
+``--impl reference`` times the reference algorithm's CPU implementation (the
+oracle port in oracle/, the reference itself being a numpy package that
+cannot travel to the GPU box) on the host cores, on a bounded sample of the
+same call, extrapolated to ms/call.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # name: (heads, t_video, t_text, d, block, grid_dims)
+    "hv": dict(heads=24, t_v=118784, t_t=256, d=128, block=128, grid=(29, 64, 64),
+               label="HunyuanVideo 720p x 129f attention (T_v 118,800 -> 118,784)"),
+    "wan": dict(heads=40, t_v=75520, t_t=0, d=128, block=128, grid=(59, 32, 40),
+                label="Wan 2.1 14B 720p x 81f self-attention (T_v 75,600 -> 75,520)"),
+    "cfg1": dict(heads=2, t_v=3840, t_t=256, d=64, block=64, grid=(1, 60, 64),
+                 label="synthetic B=1 H=2 N=4096 d=64 block=64 (reference CPU case)"),
+}
+METRIC = "sparse-attn ms/call + effective TFLOPS @ HunyuanVideo 720p shape, 90% sparsity"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="hv")
+    ap.add_argument("--sparsity", type=float, default=0.9)
+    ap.add_argument("--variant", default="sparse-rectified")
+    ap.add_argument("--kernel", default="auto", choices=["auto", "tcgen05", "simt"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-blocks", type=int, default=96)
+    ap.add_argument("--profile", action="store_true", help="fewer steps, no side legs (for ncu)")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- helpers
+
+def measured_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": d["hbm_gbs"], "bf16": d["bf16_tflops"],
+                "bf16_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]), "src": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16": 1590.0, "bf16_sustained": 1400.0, "src": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def synth_inputs(torch, cfg, heads, seed, device):
+    """gen_synthetic-style tensors (harness.py:92-126 semantics, torch RNG)."""
+    g = torch.Generator(device=device).manual_seed(seed)
+    t_v, t_t, d, B = cfg["t_v"], cfg["t_t"], cfg["d"], cfg["block"]
+    T = t_v + t_t
+    nb = t_v // B
+    # 3-D sinusoidal positional embedding of the (t, h, w) grid (harness.py:69-89)
+    t_, h_, w_ = cfg["grid"]
+    d_hw = d // 3
+    d_t = d - 2 * d_hw
+
+    def sincos(coord, dim):
+        half = dim // 2
+        freqs = torch.exp(-math.log(10000.0) * (2 * torch.arange(half + dim % 2, device=device) / max(dim, 1)))
+        ang = coord[:, None].double() * freqs[None, :].double()
+        out = torch.zeros(coord.shape[0], dim, dtype=torch.float64, device=device)
+        out[:, 0::2] = torch.sin(ang)
+        out[:, 1::2] = torch.cos(ang[:, :half])
+        return out
+
+    idx = torch.arange(t_v, device=device)
+    tt, yy, xx = idx // (h_ * w_), (idx // w_) % h_, idx % w_
+    pos = torch.cat([sincos(tt, d_t), sincos(yy, d_hw), sincos(xx, d_hw)], dim=1).float()
+    q = torch.empty(heads, T, d, dtype=torch.bfloat16, device=device)
+    k = torch.empty_like(q)
+    v = torch.empty_like(q)
+    for h in range(heads):
+        qb = torch.randn(nb, d, generator=g, device=device).repeat_interleave(B, 0)
+        kb = torch.randn(nb, d, generator=g, device=device).repeat_interleave(B, 0)
+        q[h, :t_v] = (qb + 0.3 * torch.randn(t_v, d, generator=g, device=device) + pos).bfloat16()
+        k[h, :t_v] = (kb + 0.3 * torch.randn(t_v, d, generator=g, device=device) + pos).bfloat16()
+        if t_t:
+            q[h, t_v:] = torch.randn(t_t, d, generator=g, device=device).bfloat16()
+            k[h, t_v:] = (2.0 * torch.randn(t_t, d, generator=g, device=device)).bfloat16()
+        v[h] = torch.randn(T, d, generator=g, device=device).bfloat16()
+    return q, k, v
+
+
+# ----------------------------------------------------------------------------- CPU legs
+
+def cpu_reference_sample(cfg, f, variant, sample_blocks, seed=42):
+    """Time the oracle port (the reference algorithm, numpy) on one head's
+    pooled path plus `sample_blocks` query blocks of the sparse kernel and the
+    head's text queries; extrapolate to the whole call."""
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    import numpy as np
+    from oracle import rsa_oracle as O
+    t_v, t_t, d, B = cfg["t_v"], cfg["t_t"], cfg["d"], cfg["block"]
+    if t_t:
+        qv, qt, k, v = O.gen_synthetic(seed, t_v, t_t, d, B, cfg["grid"], 1.0, 2.0, 0.3)
+    else:
+        rng = np.random.default_rng(seed)
+        qv, k, v = (rng.standard_normal((t_v, d)).astype(np.float32) for _ in range(3))
+        qt = np.zeros((0, d), np.float32)
+    qv, qt, k, v = (O.round_to_bf16(x) for x in (qv, qt, k, v))
+    t0 = time.perf_counter()
+    pooled = O.pool(qv, k, v, t_t, B)
+    imp = O.implicit_attention(pooled, d, B, t_t)
+    scores = O.pooled_scores(pooled, d)
+    g = O.gain(scores, B, pooled["lens"])
+    e = O.pooling_error(qv, k, pooled, B, d)
+    sel = O.select_mask(imp["a_pool"], f, 0.0, 0, False, pooled["n_q"])
+    _ = g > e
+    r = O.rect_factors(imp["a_pool"], sel["mask"])
+    t_pooled = time.perf_counter() - t0
+    n = pooled["n_q"]
+    rows = np.linspace(0, n - 1, min(sample_blocks, n)).astype(int)
+    t0 = time.perf_counter()
+    O.sparse_attention(qv, k, v, sel["mask"], pooled["lens"], B, query_blocks=rows)
+    t_kernel = (time.perf_counter() - t0) * n / len(rows)
+    t0 = time.perf_counter()
+    O.text_attention(qt, k, v, B)
+    t_text = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    applied = ~sel["mask"] & (g > e)
+    O.rectify(np.zeros((t_v, d), np.float32), r, imp["a_pool"], applied, pooled["v_pool"], B)
+    t_rect = time.perf_counter() - t0
+    per_head = t_pooled + t_kernel + t_text + t_rect
+    sample_s = t_pooled + t_kernel * len(rows) / n + t_text + t_rect
+    return {"ms_per_call": per_head * cfg["heads"] * 1e3, "sample_s": sample_s,
+            "per_head_s": per_head, "sample": (f"1 head (seed {seed}) of {cfg['heads']}: full pooled path + "
+                                               f"{len(rows)}/{n} query blocks of the sparse kernel + all text "
+                                               f"queries + rectification, extrapolated x{n}/{len(rows)} kernel, "
+                                               f"x{cfg['heads']} heads"),
+            "cores": os.cpu_count() or 1}
+
+
+# ----------------------------------------------------------------------------- main legs
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    f = 1.0 - args.sparsity
+    samples = []
+    for i in range(args.warmup + args.steps):
+        res = cpu_reference_sample(cfg, f, args.variant, max(8, args.cpu_sample_blocks // 4))
+        if i >= args.warmup:
+            samples.append(res)
+    ms = statistics.median(s["ms_per_call"] for s in samples)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": ms, "unit": "ms/call", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg["label"], "heads": cfg["heads"], "t_video": cfg["t_v"],
+                   "t_text": cfg["t_t"], "head_dim": cfg["d"], "block": cfg["block"],
+                   "top_k_fraction": round(f, 6), "variant": args.variant},
+        "cpu_baseline": {"value": ms, "unit": "ms/call", "cores": samples[0]["cores"], "kind": "port",
+                         "sample": samples[0]["sample"]},
+        "e2e": {"value": ms, "unit": "ms/call", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2511_19835_b200 as rsa
+    from paper_2511_19835_b200 import _native as nat
+    from paper_2511_19835_b200.pipeline import _ptr, _stream, workspace_for
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = CONFIGS[args.config]
+    f = 1.0 - args.sparsity
+    # head sharding: rank r owns heads [lo, hi)
+    per = [cfg["heads"] // world + (1 if r < cfg["heads"] % world else 0) for r in range(world)]
+    lo = sum(per[:rank])
+    heads = per[rank]
+    q, k, v = synth_inputs(torch, cfg, heads, 1234 + lo, dev)
+    T, d = q.shape[1], q.shape[2]
+    shape = nat.make_shape(heads, cfg["t_v"], cfg["t_t"], d, cfg["block"], "bfloat16", args.kernel)
+    conf = nat.make_config(f, 0.0, 0, False, args.variant)
+    grid = nat.plan(shape, conf)
+    ws = workspace_for(shape, dev)
+    out = torch.empty_like(q)
+    lib = nat.lib()
+    st = torch.cuda.current_stream()
+    sptr = _stream()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+
+    def step(record=False):
+        if record:
+            ev[0].record(st)
+        nat.check(lib.rsa_pool(C.byref(shape), _ptr(q), _ptr(k), _ptr(v), _ptr(ws), sptr))
+        if record:
+            ev[1].record(st)
+        nat.check(lib.rsa_select(C.byref(shape), C.byref(conf), _ptr(ws), sptr))
+        if record:
+            ev[2].record(st)
+        nat.check(lib.rsa_attention(C.byref(shape), C.byref(conf), _ptr(q), _ptr(k), _ptr(v), _ptr(out),
+                                    None, _ptr(ws), sptr))
+        if record:
+            ev[3].record(st)
+
+    for _ in range(args.warmup):
+        c0 = nat.last_launch_count()
+        step()
+        launches_per_step = nat.last_launch_count() - c0
+    nat.check(lib.rsa_check_device_status(_ptr(ws), sptr))
+    torch.cuda.synchronize()
+
+    # executed FLOPs of this rank (metrics.py:85 convention + text rows)
+    L = nat.layout(shape)
+    bits = ws[L["mask_bits"]:L["mask_bits"] + heads * grid.n_q * grid.n_kv].view(heads, grid.n_q, grid.n_kv)
+    mask = (bits & 1).to(torch.int64)
+    lens = torch.full((grid.n_kv,), cfg["block"], dtype=torch.int64, device=dev)
+    if grid.n_text_blocks:
+        lens[-1] = grid.last_text_block_len
+    retained_tokens = int((mask * lens[None, None, :]).sum().item())
+    flops_video = 4 * cfg["block"] * d * retained_tokens
+    flops_text = 4 * cfg["t_t"] * T * d * heads
+    flops_exec = flops_video + flops_text
+    flops_dense = 4 * T * T * d * heads
+    sparsity = 1.0 - float(mask.sum().item()) / (heads * grid.n_q * grid.n_kv)
+
+    # ---------------- timed region ----------------
+    per_stage = {"pool": [], "select": [], "attention": []}
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(st)
+        for _ in range(args.steps):
+            step(record=False)
+        t1.record(st)
+        torch.cuda.synchronize()
+        # per-kernel split, measured on the launching stream in separate steps
+        for _ in range(max(2, min(args.steps, 5))):
+            step(record=True)
+            torch.cuda.synchronize()
+            per_stage["pool"].append(ev[0].elapsed_time(ev[1]))
+            per_stage["select"].append(ev[1].elapsed_time(ev[2]))
+            per_stage["attention"].append(ev[2].elapsed_time(ev[3]))
+    if world > 1:
+        dist.barrier()
+    total_ms = t0.elapsed_time(t1)
+    ms_step = total_ms / args.steps
+    stage = {k2: statistics.median(vv) for k2, vv in per_stage.items()}
+    if world > 1:
+        tt = torch.tensor([ms_step, stage["attention"], stage["pool"], stage["select"]], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_step, stage["attention"], stage["pool"], stage["select"] = tt.tolist()
+        ft = torch.tensor([flops_exec, flops_dense], dtype=torch.float64, device=dev)
+        dist.all_reduce(ft)
+        flops_exec, flops_dense = ft.tolist()
+
+    # ---------------- end-to-end through the public API (host buffers) ----------------
+    e2e = None
+    if not args.profile and args.e2e_steps > 0:
+        hq, hk, hv = (x.cpu().pin_memory() for x in (q, k, v))
+        hout = torch.empty(q.shape, dtype=q.dtype).pin_memory()
+        dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+
+        def e2e_step():
+            dq.copy_(hq, non_blocking=True)
+            dk.copy_(hk, non_blocking=True)
+            dv.copy_(hv, non_blocking=True)
+            o = rsa.rectified_sparse_attention(dq[None], dk[None], dv[None], num_text_tokens=cfg["t_t"],
+                                               block=cfg["block"], top_k_fraction=f, variant=args.variant,
+                                               kernel=args.kernel, workspace=ws)
+            hout.copy_(o[0], non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record(st)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        a1.record(st)
+        torch.cuda.synchronize()
+        e2e_ms = a0.elapsed_time(a1) / args.e2e_steps
+        if world > 1:
+            tt = torch.tensor([e2e_ms], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_ms = tt.item()
+        nbytes = q.numel() * q.element_size()
+        e2e = {"value": e2e_ms, "unit": "ms/call", "h2d_bytes_per_step": 3 * nbytes * world,
+               "d2h_bytes_per_step": nbytes * world,
+               "path": "pinned host q/k/v -> H2D -> rectified_sparse_attention -> D2H output"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    peaks = measured_peaks()
+    attn_ms = stage["attention"]
+    per_rank_exec = flops_exec / world
+    achieved = per_rank_exec / (attn_ms * 1e-3) / 1e12
+    peak = peaks["bf16_sustained"]
+    traffic = None
+    tp = ROOT / "profiles" / "attn_traffic.json"
+    if tp.exists():
+        try:
+            traffic = json.loads(tp.read_text()).get(args.config)
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC, "value": ms_step, "unit": "ms/call", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (gen_synthetic-style, torch RNG)",
+        "config": {"workload": cfg["label"], "heads": cfg["heads"], "t_video": cfg["t_v"], "t_text": cfg["t_t"],
+                   "head_dim": d, "block": cfg["block"], "top_k_fraction": round(f, 6),
+                   "weight_threshold": 0.0, "adjacency_radius": 0, "force_text_blocks": False,
+                   "variant": args.variant, "parallelism": f"head-sharded x{world}",
+                   "l2": "inputs 2.2 GB >> 126 MB L2 (no flush needed)" if args.config != "cfg1"
+                   else "inputs 6 MB; L2 resident", "kernel": args.kernel},
+        "tflops_effective": flops_exec / (ms_step * 1e-3) / 1e12,
+        "tflops_dense_equivalent": flops_dense / (ms_step * 1e-3) / 1e12,
+        "realized_sparsity": sparsity,
+        "kernels_ms": stage,
+        "roofline": {"bound": "tensor", "kernel": "attn_tc_kernel (K3+K4)", "achieved": achieved,
+                     "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                     "frac_of_burst": achieved / peaks["bf16"], "peak_src": peaks["src"] + " sustained",
+                     "traffic": traffic,
+                     "algorithmic": f"{per_rank_exec / 1e12:.3f} TFLOP executed per launch "
+                                    f"(4*B*d*sum(mask*len) + 4*T_t*T*d)"},
+        "gpu_launches": launches_per_step * args.steps,
+        "e2e": e2e,
+    }
+    if not args.profile:
+        line["clocks"] = clocks.summary()
+    if world == 1 and not args.no_cpu_baseline and not args.profile:
+        cb = cpu_reference_sample(cfg, f, args.variant, args.cpu_sample_blocks)
+        line["cpu_baseline"] = {"value": cb["ms_per_call"], "unit": "ms/call", "cores": cb["cores"],
+                                "kind": "port", "sample": cb["sample"], "sample_s": cb["sample_s"]}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -251,3 +251,55 @@ def test_errors_map_to_reference_classes():
     qv, qt, k, v = O.random_problem(0, t_v=8, t_t=0, d=8)
     with pytest.raises(rsa.ConfigError):
         run_np(qv, qt, k, v, 4, 0.2, 0.3, 1, True, "bogus")
+
+
+# ---------------------------------------------------------------- tcgen05 kernel
+
+@pytest.mark.parametrize("d,block", [(64, 64), (64, 128), (128, 64), (128, 128)])
+@pytest.mark.parametrize("t_t", [0, 200])
+def test_tcgen05_kernel_matches_oracle_and_simt(d, block, t_t):
+    """The tensor-core K3 against the fp32 oracle pipeline and the CUDA-core
+    K3 on bf16-valued inputs: ragged text tile and ragged last kv block
+    (t_t = 200), odd query-block count for B = 64, all retained lists."""
+    heads = 2
+    t_v = block * (23 if block == 64 else 12)
+    rng = np.random.default_rng(d + block + t_t)
+    per_head = []
+    for h in range(heads):
+        qv, qt, k, v = O.gen_synthetic(100 + h, t_v, max(t_t, 1), d, block, (1, 1, t_v), 1.0, 2.0, 0.3)
+        qt, k, v = qt[:t_t], k[:t_v + t_t], v[:t_v + t_t]
+        per_head.append(tuple(O.round_to_bf16(x) for x in (qv, qt, k, v)))
+    q = torch.stack([torch.cat([to_bf16_tensor(a), to_bf16_tensor(b)]) for a, b, _, _ in per_head])
+    k = torch.stack([to_bf16_tensor(x[2]) for x in per_head])
+    v = torch.stack([to_bf16_tensor(x[3]) for x in per_head])
+    outs = {}
+    for kern in ("tcgen05", "simt"):
+        lse = torch.empty(heads, t_v + t_t, dtype=torch.float32, device="cuda")
+        outs[kern] = (rsa.rectified_sparse_attention(q, k, v, num_text_tokens=t_t, block=block,
+                                                     top_k_fraction=0.2, weight_threshold=0.3,
+                                                     adjacency_radius=1, force_text_blocks=True,
+                                                     kernel=kern, lse=lse, check_status=True), lse)
+    diff = (outs["tcgen05"][0].float() - outs["simt"][0].float()).abs().max().item()
+    assert diff <= 1e-2, diff
+    lse_diff = (outs["tcgen05"][1] - outs["simt"][1]).abs().max().item()
+    assert lse_diff <= 1e-2, lse_diff
+    for h, (qv, qt, kk, vv) in enumerate(per_head):
+        ref = O.pipeline(qv, qt, kk, vv, block, 0.2, 0.3, 1, True, "sparse-rectified")
+        assert_bf16_close(outs["tcgen05"][0][h], np.concatenate([ref["o_video"], ref["o_text"]]), f"head {h}")
+        np.testing.assert_allclose(outs["tcgen05"][1][h, :t_v].cpu().numpy(), ref["lse"], atol=2e-2, rtol=0)
+
+
+def test_tcgen05_unrectified_block_sparse_seam():
+    """kernel-only seam (kernel.py:65-117) on the tensor-core kernel vs the fp64
+    masked oracle, bf16-valued inputs."""
+    rng = np.random.default_rng(11)
+    block, d, t_v, t_t = 128, 128, 128 * 10, 77
+    qv, qt, k, v = (O.round_to_bf16(x) for x in O.random_problem(5, t_v=t_v, t_t=t_t, d=d, dtype=np.float32))
+    n, m, last = O.block_geometry(t_v, t_t, block)
+    mask = rng.random((n, m)) < 0.35
+    mask[np.arange(n), np.arange(n)] = True
+    grid = partition(AttentionProblem(q_video=qv, q_text=qt, k=k, v=v, d=d, block=block))
+    out, _ = rsa.block_sparse_attention(to_bf16_tensor(qv), to_bf16_tensor(k), to_bf16_tensor(v),
+                                        mask, grid, kernel="tcgen05")
+    _, expected = O.masked_attention_fp64(qv, k, v, mask, O.kv_lengths(n, m, block, last), block)
+    assert_bf16_close(out, expected, "seam")
