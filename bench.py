@@ -94,6 +94,23 @@ class ClockSampler:
         self._t = threading.Thread(target=self._run, daemon=True)
 
     def _run(self):
+        try:  # NVML at 20 ms when available (nvidia-smi is too slow for sub-second regions)
+            import pynvml as nv
+            nv.nvmlInit()
+            hd = nv.nvmlDeviceGetHandleByIndex(self.index)
+            bits = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                    "sw_power_cap": 0x4}
+            mx = nv.nvmlDeviceGetMaxClockInfo(hd, nv.NVML_CLOCK_SM)
+            while not self._stop.is_set():
+                sm = nv.nvmlDeviceGetClockInfo(hd, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(hd)
+                self.rows.append([str(self.index), str(sm), str(mx), "", ""] +
+                                 ["Active" if r & bits[k] else "Not Active" for k in
+                                  ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")])
+                self._stop.wait(0.02)
+            return
+        except Exception:
+            pass
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",

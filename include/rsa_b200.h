@@ -100,6 +100,7 @@ typedef struct {
   size_t kv_list;     /* i32 [N][M]    ascending retained kv block ids               */
   size_t tile_count;  /* i32 [tiles]   kv entries per 128-row tcgen05 tile           */
   size_t tile_list;   /* i32 [tiles][M] (kv id | member bits << 24)                  */
+  size_t v_t;         /* bf16 [d][T]   V transposed (tcgen05 path: K-major PV operand) */
   size_t status;      /* i32 [4]       device status flags (degenerate row, ...)     */
   size_t total;
 } rsa_workspace_layout;

@@ -17,8 +17,8 @@
 //                 step ahead, so it runs while softmax works on S_{j-1}
 //                 O  += P_j V_j  (TS: P_j read straight from TMEM)
 //   warp 2      TMEM allocation / release
-//   warps 4-7   softmax: one query row per thread (TMEM lane), fp32 online
-//               softmax in the log2 domain with lazy (threshold 2^8) O
+//   warps 4-11  softmax: two threads per query row (TMEM lane), each owning
+//               half of the score columns; fp32 online softmax in the log2 domain with lazy (threshold 2^8) O
 //               rescaling, P packed to bf16 back into the S columns; then the
 //               epilogue O / l * R_n + comp_n -> bf16 store, LSE.
 // TMEM columns: S0 [0,B), S1 [B,2B), O [2B, 2B+D).
@@ -26,61 +26,95 @@
 #include "tc_ptx.cuh"
 
 #include <cuda.h>
+#include <cstdlib>
 #include <cudaTypedefs.h>
 
 namespace rsa {
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kNst = 4;                 // K/V ring stages
+constexpr int kThreads = 384;   // 4 control warps + 8 softmax warps
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale O only if max grows by > 2^8
 
-template <int D, int BKV>
+template <int D, int BKV, bool QTM, bool VT>
 struct Cfg {
+  // S/P TMEM buffers: 3 when Q stays in shared memory, so S_{j+1} never
+  // overwrites the buffer PV_{j-1} is still reading (a TMEM WAR hazard that
+  // drains the tensor pipe every step); 2 when Q lives in TMEM
+  static constexpr int NS = QTM ? 2 : 3;
+  // K/V ring depth: Q in TMEM frees its 32 KB of shared memory for 2 more stages
+  static constexpr int NST = BKV * D * 2 <= 16384 ? 8 : (QTM ? 6 : 5);
   static constexpr int PANELS = D / 64;
   static constexpr int Q_PANEL = 128 * 128;     // bytes: 128 rows x 128 B
   static constexpr int KV_PANEL = BKV * 128;    // bytes: B rows x 128 B
   static constexpr int Q_BYTES = 128 * D * 2;
   static constexpr int STAGE = BKV * D * 2;
-  static constexpr int O_COL = 2 * BKV;
-  static constexpr int TMEM_COLS = (2 * BKV + D) <= 256 ? 256 : 512;
-  static constexpr int SMEM = 1024 + Q_BYTES + kNst * STAGE + 256;
+  static constexpr int O_COL = NS * BKV;
+  static constexpr int Q_COL = NS * BKV + D;      // Q (bf16 pairs) when resident in TMEM
+  static constexpr int TMEM_USED = NS * BKV + D + (QTM ? D / 2 : 0);
+  static constexpr int TMEM_COLS = TMEM_USED <= 256 ? 256 : 512;
+  static constexpr int Q_SMEM = QTM ? 0 : Q_BYTES;
+  static constexpr int SMEM = 1024 + Q_SMEM + NST * STAGE + 256 + 768 * 4;
   static constexpr uint32_t IDESC_S = ptx::idesc_bf16(128, BKV, false);
-  static constexpr uint32_t IDESC_O = ptx::idesc_bf16(128, D, true);
+  // PV B operand: V^T tiles (K-major) or V tiles (MN-major)
+  static constexpr uint32_t IDESC_O = ptx::idesc_bf16(128, D, !VT);
+  static constexpr int VT_PANEL = D * 128;      // bytes: D rows (head dims) x 128 B (64 keys)
 };
 
 struct TcParams {
   Geometry g;
   Workspace ws;
   __nv_bfloat16* out;
+  const __nv_bfloat16* q;
   float* lse;
   int rectify;
   int64_t n_text_tiles;
   int64_t text_tiles_per_head;
   int64_t video_tiles_per_head;
   float scale_log2;  // log2(e) / sqrt(d)
+  int trace_cta;     // CTA traced per step when stamps == 2
+  int stamps;        // RSA_TC_STAMPS=1: per-CTA globaltimer stamps into `lse` (profiling)
+  int mode;          // 0 normal; diagnostics: 1 no softmax math, 2 TMA only, 3 MMA only, 4 MMA+TMA,
+                     // 6 softmax only, 7 normal + per-CTA globaltimer stamps into `lse`
 };
 
-template <int D, int BKV>
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <int D, int BKV, bool QTM, bool VT, int EMU>
 __global__ void __launch_bounds__(kThreads, 1)
 attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                const __grid_constant__ CUtensorMap tm_v, const TcParams P) {
-  using C = Cfg<D, BKV>;
+  using C = Cfg<D, BKV, QTM, VT>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* q_s = base;
-  uint8_t* kv_s = base + C::Q_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(kv_s + kNst * C::STAGE);
+  uint8_t* kv_s = base + C::Q_SMEM;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(kv_s + C::NST * C::STAGE);
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;
-  uint64_t* kv_empty = kv_full + kNst;
-  uint64_t* s_full = kv_empty + kNst;      // [2]
-  uint64_t* p_full = s_full + 2;           // [2]
-  uint64_t* pv_done = p_full + 2;          // [1]
+  uint64_t* kv_empty = kv_full + C::NST;
+  uint64_t* s_full = kv_empty + C::NST;    // [NS]
+  uint64_t* p_full = s_full + C::NS;       // [NS]
+  uint64_t* pv_done = p_full + C::NS;      // [1]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 1);
+  float* red_max = reinterpret_cast<float*>(bars + 32);   // [2][2][128] row maxima + [2][128] row sums
 
   const Geometry& g = P.g;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  unsigned long long* tstamp =
+      (P.stamps && P.lse) ? reinterpret_cast<unsigned long long*>(P.lse) + blockIdx.x * 8 : nullptr;
+  // per-step clock64 trace of one CTA (P.stamps == 2): [step][8] after the per-CTA stamps
+  long long* trace = (P.stamps == 2 && P.lse && blockIdx.x == (unsigned)P.trace_cta)
+                         ? reinterpret_cast<long long*>(P.lse) + (int64_t)gridDim.x * 8 : nullptr;
+  if (tstamp && threadIdx.x == 0) {
+    tstamp[0] = gtimer();
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    tstamp[7] = smid;
+  }
 
   // ---- tile decode (LPT order: text tiles first) ----
   const int64_t bid = blockIdx.x;
@@ -104,14 +138,14 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   }
 
   if (threadIdx.x == 0) {
-    ptx::mbar_init(q_full, 1);
-    for (int i = 0; i < kNst; ++i) {
+    ptx::mbar_init(q_full, QTM ? 256 : 1);
+    for (int i = 0; i < C::NST; ++i) {
       ptx::mbar_init(kv_full + i, 1);
       ptx::mbar_init(kv_empty + i, 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < C::NS; ++i) {
       ptx::mbar_init(s_full + i, 1);
-      ptx::mbar_init(p_full + i, 128);
+      ptx::mbar_init(p_full + i, 256);
     }
     ptx::mbar_init(pv_done, 1);
     ptx::fence_barrier_init();
@@ -121,29 +155,37 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (tstamp && threadIdx.x == 0) tstamp[1] = gtimer();
 
   if (warp == 0) {
     // ===================== TMA producer =====================
-    if (lane == 0 && count > 0) {
+    if (lane == 0 && count > 0 && P.mode != 3 && P.mode != 6) {
       ptx::prefetch_tmap(&tm_q);
       ptx::prefetch_tmap(&tm_k);
       ptx::prefetch_tmap(&tm_v);
-      ptx::mbar_expect_tx(q_full, C::Q_BYTES);
-#pragma unroll
-      for (int p = 0; p < C::PANELS; ++p)
-        ptx::tma_load_3d(q_s + p * C::Q_PANEL, &tm_q, q_full, 64 * p, (int)q_row0, (int)h);
-      int it = 0;
-      auto load = [&](int64_t j, bool is_v) {
-        const int s = it % kNst;
-        const uint32_t ph = (it / kNst) & 1;
-        const int64_t m = list ? (list[j] & 0xFFFFFF) : j;
-        ptx::mbar_wait(kv_empty + s, ph ^ 1);
-        ptx::mbar_expect_tx(kv_full + s, C::STAGE);
-        uint8_t* dst = kv_s + s * C::STAGE;
+      if (!QTM) {
+        ptx::mbar_expect_tx(q_full, C::Q_BYTES);
 #pragma unroll
         for (int p = 0; p < C::PANELS; ++p)
-          ptx::tma_load_3d(dst + p * C::KV_PANEL, is_v ? &tm_v : &tm_k, kv_full + s, 64 * p,
-                           (int)(m * g.B), (int)h);
+          ptx::tma_load_3d(q_s + p * C::Q_PANEL, &tm_q, q_full, 64 * p, (int)q_row0, (int)h);
+      }
+      int it = 0;
+      auto load = [&](int64_t j, bool is_v) {
+        const int s = it % C::NST;
+        const uint32_t ph = (it / C::NST) & 1;
+        const int64_t m = list ? (list[j] & 0xFFFFFF) : j;
+        ptx::mbar_wait(kv_empty + s, ph ^ 1);
+        if (trace && j < 64) trace[j * 8 + (is_v ? 7 : 6)] = clock64();
+        ptx::mbar_expect_tx(kv_full + s, C::STAGE);
+        uint8_t* dst = kv_s + s * C::STAGE;
+        const int panels = (is_v && VT) ? BKV / 64 : C::PANELS;
+        for (int p = 0; p < panels; ++p)
+          if (is_v && VT)   // V^T: box (64 keys, D dims) per 64-key panel
+            ptx::tma_load_3d(dst + p * C::VT_PANEL, &tm_v, kv_full + s, (int)(m * g.B) + 64 * p, 0, (int)h);
+          else if (is_v)    // V: box (64 dims, B keys) per 64-dim panel
+            ptx::tma_load_3d(dst + p * C::KV_PANEL, &tm_v, kv_full + s, 64 * p, (int)(m * g.B), (int)h);
+          else
+            ptx::tma_load_3d(dst + p * C::KV_PANEL, &tm_k, kv_full + s, 64 * p, (int)(m * g.B), (int)h);
         ++it;
       };
       for (int64_t j = 0; j <= count; ++j) {
@@ -153,39 +195,65 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
-    if (lane == 0 && count > 0) {
+    if (lane == 0 && count > 0 && P.mode == 6) {
+      // diagnostic: softmax alone -- hand out S buffers without any MMA
+      for (int64_t j = 0; j < count; ++j) {
+        if (j >= 1) {
+          ptx::mbar_wait(p_full + ((j - 1) % C::NS), (uint32_t)(((j - 1) / C::NS) & 1));
+          ptx::tc_commit(pv_done);          // "PV_{j-1}" done: one phase per step
+        }
+        ptx::tc_commit(s_full + (j % C::NS));
+      }
+      ptx::mbar_wait(p_full + ((count - 1) % C::NS), (uint32_t)(((count - 1) / C::NS) & 1));
+      ptx::tc_commit(pv_done);
+    } else if (lane == 0 && count > 0 && P.mode == 2) {
+      // diagnostic: consume the K/V stream without any MMA (TMA rate only)
+      for (int it = 0; it < 2 * count; ++it) {
+        ptx::mbar_wait(kv_full + it % C::NST, (it / C::NST) & 1);
+        ptx::mbar_arrive(kv_empty + it % C::NST);
+      }
+    } else if (lane == 0 && count > 0) {
       ptx::mbar_wait(q_full, 0);
       ptx::tc_fence_after();
+      if (tstamp) tstamp[2] = gtimer();
       const uint32_t q_addr = ptx::smem_u32(q_s);
       const uint32_t kv_addr = ptx::smem_u32(kv_s);
       int it = 0;
       for (int64_t j = 0; j <= count; ++j) {
         if (j < count) {
-          const int s = it % kNst;
-          ptx::mbar_wait(kv_full + s, (it / kNst) & 1);
+          const int s = it % C::NST;
+          if (P.mode != 3) ptx::mbar_wait(kv_full + s, (it / C::NST) & 1);
+          if (trace && j < 64) trace[j * 8 + 0] = clock64();
           ptx::tc_fence_after();
-          const uint32_t d_tmem = tmem + (uint32_t)((j & 1) * BKV);
+          const uint32_t d_tmem = tmem + (uint32_t)((j % C::NS) * BKV);
 #pragma unroll
           for (int k = 0; k < D / 16; ++k) {
             const uint32_t off = (uint32_t)((k % 4) * 32);   // 16 bf16 = 32 B inside the 128 B row
-            const uint64_t a = ptx::sw128_desc(q_addr + (k / 4) * C::Q_PANEL + off, 16, 1024);
             const uint64_t b = ptx::sw128_desc(kv_addr + s * C::STAGE + (k / 4) * C::KV_PANEL + off, 16, 1024);
-            ptx::mma_ss(d_tmem, a, b, C::IDESC_S, k > 0);
+            if (QTM) {
+              ptx::mma_ts(d_tmem, tmem + C::Q_COL + k * 8, b, C::IDESC_S, k > 0);
+            } else {
+              const uint64_t a = ptx::sw128_desc(q_addr + (k / 4) * C::Q_PANEL + off, 16, 1024);
+              ptx::mma_ss(d_tmem, a, b, C::IDESC_S, k > 0);
+            }
           }
           ptx::tc_commit(kv_empty + s);
-          ptx::tc_commit(s_full + (j & 1));
+          ptx::tc_commit(s_full + (j % C::NS));
           ++it;
         }
         if (j >= 1) {
           const int64_t jj = j - 1;
-          ptx::mbar_wait(p_full + (jj & 1), (uint32_t)((jj >> 1) & 1));
-          const int s = it % kNst;
-          ptx::mbar_wait(kv_full + s, (it / kNst) & 1);
+          if (P.mode < 3) ptx::mbar_wait(p_full + (jj % C::NS), (uint32_t)((jj / C::NS) & 1));
+          if (trace && jj < 64) trace[jj * 8 + 1] = clock64();
+          const int s = it % C::NST;
+          if (P.mode != 3) ptx::mbar_wait(kv_full + s, (it / C::NST) & 1);
+          if (trace && jj < 64) trace[jj * 8 + 2] = clock64();
           ptx::tc_fence_after();
-          const uint32_t a_tmem = tmem + (uint32_t)((jj & 1) * BKV);
+          const uint32_t a_tmem = tmem + (uint32_t)((jj % C::NS) * BKV);
 #pragma unroll
           for (int k = 0; k < BKV / 16; ++k) {
-            const uint64_t b = ptx::sw128_desc(kv_addr + s * C::STAGE + k * 2048, C::KV_PANEL, 1024);
+            const uint64_t b = VT ? ptx::sw128_desc(kv_addr + s * C::STAGE + (k / 4) * C::VT_PANEL + (k % 4) * 32, 16, 1024)
+                                  : ptx::sw128_desc(kv_addr + s * C::STAGE + k * 2048, C::KV_PANEL, 1024);
             ptx::mma_ts(tmem + C::O_COL, a_tmem + k * 8, b, C::IDESC_O, (jj > 0 || k > 0) ? 1u : 0u);
           }
           ptx::tc_commit(kv_empty + s);
@@ -193,16 +261,46 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           ++it;
         }
       }
+      if (P.mode >= 3 && P.mode <= 4) ptx::mbar_wait(pv_done, (uint32_t)((count - 1) & 1));
+      if (tstamp) tstamp[3] = gtimer();
     }
   } else if (warp >= 4) {
     // ===================== softmax + epilogue =====================
-    const int quad = warp - 4;
+    // Two warps per TMEM lane quadrant: `half` 0 owns columns [0, B/2) of its
+    // 32 rows, half 1 columns [B/2, B); the row maximum is exchanged through
+    // shared memory once per step, the row sum only at the end.
+    constexpr int HC = BKV / 2;     // score columns per thread
+    constexpr int HD = D / 2;       // output columns per thread
+    const int sw = warp - 4;
+    const int quad = sw & 3, half = sw >> 2;
     const int row = quad * 32 + lane;
     const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
     const int sub = row / (int)g.B;          // which member query block of the tile
-    float m_run = -INFINITY, l_run = 0.f;
+    float m_run = -INFINITY, l_part = 0.f;
     const float sl2 = P.scale_log2;
-    for (int64_t j = 0; j < count; ++j) {
+    if (QTM && count > 0) {
+      // Q row -> TMEM lanes (A operand of S = Q K^T): this thread packs half
+      // of its row's d columns, bf16 pairs per 32-bit column
+      constexpr int QW = D / 4;                 // 32-bit words per thread
+      uint32_t qw[QW];
+      const int64_t grow = q_row0 + row;
+      const uint4* src = reinterpret_cast<const uint4*>(P.q + (h * g.T + grow) * D + half * (D / 2));
+#pragma unroll
+      for (int i = 0; i < QW / 4; ++i) {
+        const uint4 x = grow < g.T ? __ldg(src + i) : make_uint4(0, 0, 0, 0);
+        qw[4 * i] = x.x; qw[4 * i + 1] = x.y; qw[4 * i + 2] = x.z; qw[4 * i + 3] = x.w;
+      }
+      if constexpr (QW == 32) {
+        ptx::tmem_st32(lane_base + C::Q_COL + half * QW, qw);
+      } else {
+        ptx::tmem_st16(lane_base + C::Q_COL + half * QW, qw);
+      }
+      ptx::tmem_st_wait();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(q_full);
+    }
+    const int64_t sm_count = (P.mode >= 2 && P.mode <= 4) ? 0 : count;
+    for (int64_t j = 0; j < sm_count; ++j) {
       int64_t m;
       bool member;
       if (list) {
@@ -214,23 +312,35 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         member = true;
       }
       const int len = (m == g.M - 1 && g.n_text > 0) ? (int)g.last_len : (int)g.B;
-      ptx::mbar_wait(s_full + (j & 1), (uint32_t)((j >> 1) & 1));
+      ptx::mbar_wait(s_full + (j % C::NS), (uint32_t)((j / C::NS) & 1));
+      if (trace && sw == 0 && lane == 0 && j < 64) trace[j * 8 + 3] = clock64();
       ptx::tc_fence_after();
-      const uint32_t s_addr = lane_base + (uint32_t)((j & 1) * BKV);
-      uint32_t sr[BKV / 32][32];
+      if (P.mode == 1) {  // diagnostic: no softmax math
+        ptx::mbar_arrive(p_full + (j % C::NS));
+        continue;
+      }
+      const uint32_t s_addr = lane_base + (uint32_t)((j % C::NS) * BKV);
+      uint32_t sr[HC / 32][32];
 #pragma unroll
-      for (int c = 0; c < BKV / 32; ++c) ptx::tmem_ld32(s_addr + c * 32, sr[c]);
+      for (int c = 0; c < HC / 32; ++c) ptx::tmem_ld32(s_addr + half * HC + c * 32, sr[c]);
       ptx::tmem_ld_wait();
-      float mx = -INFINITY;
+      if (!member || len < BKV) {
 #pragma unroll
-      for (int c = 0; c < BKV / 32; ++c)
+        for (int c = 0; c < HC / 32; ++c)
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          float s = __uint_as_float(sr[c][i]);
-          if (!member || c * 32 + i >= len) s = -INFINITY;
-          sr[c][i] = __float_as_uint(s);
-          mx = fmaxf(mx, s);
-        }
+          for (int i = 0; i < 32; ++i)
+            if (!member || half * HC + c * 32 + i >= len) sr[c][i] = __float_as_uint(-INFINITY);
+      }
+      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int c = 0; c < HC / 32; ++c)
+#pragma unroll
+        for (int i = 0; i < 32; ++i) mx4[i & 3] = fmaxf(mx4[i & 3], __uint_as_float(sr[c][i]));
+      float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+      red_max[(j & 1) * 256 + half * 128 + row] = mx;
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (trace && sw == 0 && lane == 0 && j < 64) trace[j * 8 + 4] = clock64();
+      mx = fmaxf(mx, red_max[(j & 1) * 256 + (half ^ 1) * 128 + row]);
       const float m_blk = mx * sl2;              // -inf if the row retains nothing here
       const float m_old = m_run;
       float alpha = 1.f;
@@ -241,20 +351,24 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         m_run = m_blk;
       }
       const float base_m = (m_run == -INFINITY) ? 0.f : m_run;
-      float sum = 0.f;
+      float sum4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int c = 0; c < BKV / 32; ++c) {
+      for (int c = 0; c < HC / 32; ++c) {
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float p0 = ptx::ex2(fmaf(__uint_as_float(sr[c][2 * i]), sl2, -base_m));
-          const float p1 = ptx::ex2(fmaf(__uint_as_float(sr[c][2 * i + 1]), sl2, -base_m));
-          sum += p0 + p1;
+          // EMU of every 8 element pairs go to the FMA pipe, the rest to MUFU
+          const bool emu = (i & 7) < EMU;
+          const float x0 = fmaf(__uint_as_float(sr[c][2 * i]), sl2, -base_m);
+          const float x1 = fmaf(__uint_as_float(sr[c][2 * i + 1]), sl2, -base_m);
+          const float p0 = emu ? ptx::ex2_poly(x0) : ptx::ex2(x0);
+          const float p1 = emu ? ptx::ex2_poly(x1) : ptx::ex2(x1);
+          sum4[i & 3] += p0 + p1;
           pk[i] = ptx::pack_bf16(p0, p1);
         }
-        ptx::tmem_st16(s_addr + c * 16, pk);
+        ptx::tmem_st16(s_addr + half * (HC / 2) + c * 16, pk);
       }
-      l_run = l_run * alpha + sum;
+      l_part = l_part * alpha + ((sum4[0] + sum4[1]) + (sum4[2] + sum4[3]));
       // tcgen05.ld/st are warp-collective (.sync.aligned): the correction runs
       // for the whole warp whenever any of its rows needs it
       if (__any_sync(0xffffffffu, rescale_o)) {
@@ -263,22 +377,28 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         ptx::tc_fence_after();
         const float a = rescale_o ? alpha : 1.f;
 #pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
+        for (int c = 0; c < HD / 32; ++c) {
           uint32_t o[32];
-          ptx::tmem_ld32(lane_base + C::O_COL + c * 32, o);
+          const uint32_t oa = lane_base + C::O_COL + half * HD + c * 32;
+          ptx::tmem_ld32(oa, o);
           ptx::tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * a);
-          ptx::tmem_st32(lane_base + C::O_COL + c * 32, o);
+          ptx::tmem_st32(oa, o);
         }
       }
       ptx::tmem_st_wait();
       ptx::tc_fence_before();
-      ptx::mbar_arrive(p_full + (j & 1));
+      if (trace && sw == 0 && lane == 0 && j < 64) trace[j * 8 + 5] = clock64();
+      ptx::mbar_arrive(p_full + (j % C::NS));
     }
 
     // ---- epilogue: O / l, rectification (rectify.py:66-89), bf16 store, LSE ----
-    if (count > 0) {
+    if (tstamp && sw == 0 && lane == 0) tstamp[4] = gtimer();
+    red_max[512 + half * 128 + row] = l_part;
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    const float l_run = l_part + red_max[512 + (half ^ 1) * 128 + row];
+    if (sm_count > 0) {
       ptx::mbar_wait(pv_done, (uint32_t)((count - 1) & 1));
       ptx::tc_fence_after();
     }
@@ -294,9 +414,10 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     const float inv_l = (count > 0 && l_run > 0.f) ? 1.f / l_run : 0.f;
     __nv_bfloat16* orow = P.out + (h * g.T + grow) * D;
 #pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
+    for (int c = 0; c < HD / 32; ++c) {
       uint32_t o[32];
-      ptx::tmem_ld32(lane_base + C::O_COL + c * 32, o);
+      const int col0 = half * HD + c * 32;
+      ptx::tmem_ld32(lane_base + C::O_COL + col0, o);
       ptx::tmem_ld_wait();
       if (valid) {
 #pragma unroll
@@ -304,7 +425,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           uint32_t w[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            const int col = c * 32 + v8 * 8 + 2 * i;
+            const int col = col0 + v8 * 8 + 2 * i;
             float y0 = inv_l == 0.f ? 0.f : __uint_as_float(o[v8 * 8 + 2 * i]) * inv_l * rfac;
             float y1 = inv_l == 0.f ? 0.f : __uint_as_float(o[v8 * 8 + 2 * i + 1]) * inv_l * rfac;
             if (comp) {
@@ -313,22 +434,54 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
             }
             w[i] = ptx::pack_bf16(y0, y1);
           }
-          *reinterpret_cast<uint4*>(orow + c * 32 + v8 * 8) = make_uint4(w[0], w[1], w[2], w[3]);
+          *reinterpret_cast<uint4*>(orow + col0 + v8 * 8) = make_uint4(w[0], w[1], w[2], w[3]);
         }
       }
     }
-    if (valid && P.lse)
+    if (tstamp && sw == 0 && lane == 0) tstamp[5] = gtimer();
+    if (valid && half == 0 && P.lse && !tstamp)
       P.lse[h * g.T + grow] = l_run > 0.f ? (log2f(l_run) + m_run) * 0.69314718055994531f : -INFINITY;
   }
 
   __syncwarp();
   ptx::tc_fence_before();
   __syncthreads();
+  if (tstamp && threadIdx.x == 0) tstamp[6] = gtimer();
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<C::TMEM_COLS>(tmem);
   }
 }
+
+// V [H][T][d] -> V^T [H][d][T] through a padded 64x64 shared-memory tile
+__global__ void __launch_bounds__(256) transpose_v_kernel(const __nv_bfloat16* __restrict__ v,
+                                                          __nv_bfloat16* __restrict__ vt, int64_t T,
+                                                          int64_t pitch, int64_t d) {
+  __shared__ __nv_bfloat16 tile[64][72];
+  const int64_t h = blockIdx.z, t0 = (int64_t)blockIdx.x * 64, c0 = (int64_t)blockIdx.y * 64;
+  const __nv_bfloat16* src = v + h * T * d;
+  for (int i = threadIdx.x; i < 64 * 8; i += 256) {
+    const int r = i / 8, cc = (i % 8) * 8;
+    uint4 x = make_uint4(0, 0, 0, 0);
+    if (t0 + r < T) x = __ldg(reinterpret_cast<const uint4*>(src + (t0 + r) * d + c0 + cc));
+    *reinterpret_cast<uint4*>(&tile[r][cc]) = x;
+  }
+  __syncthreads();
+  __nv_bfloat16* dst = vt + h * d * pitch;
+  for (int i = threadIdx.x; i < 64 * 8; i += 256) {
+    const int c = i / 8, rr = (i % 8) * 8;
+    if (t0 + rr + 8 <= T) {
+      __align__(16) __nv_bfloat16 w[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) w[k] = tile[rr + k][c];
+      *reinterpret_cast<uint4*>(dst + (c0 + c) * pitch + t0 + rr) = *reinterpret_cast<const uint4*>(w);
+    } else {
+      for (int k = 0; k < 8 && t0 + rr + k < T; ++k) dst[(c0 + c) * pitch + t0 + rr + k] = tile[rr + k][c];
+    }
+  }
+}
+
+int64_t vt_pitch(const Geometry& g) { return (g.T + 7) / 8 * 8; }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -342,12 +495,15 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-bool make_tmap(CUtensorMap* tm, const void* ptr, const Geometry& g, int box_rows) {
+// 3-D bf16 tensor [dim2][dim1][dim0] (dim0 contiguous), box (64, box1, 1), 128B swizzle
+bool make_tmap_3d(CUtensorMap* tm, const void* ptr, int64_t dim0, int64_t dim1, int64_t dim2, int box1,
+                  int64_t pitch0 = 0) {
   auto fn = encode_fn();
   if (!fn) return false;
-  cuuint64_t dims[3] = {(cuuint64_t)g.d, (cuuint64_t)g.T, (cuuint64_t)g.H};
-  cuuint64_t strides[2] = {(cuuint64_t)g.d * 2, (cuuint64_t)g.T * g.d * 2};
-  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
+  if (pitch0 == 0) pitch0 = dim0;
+  cuuint64_t dims[3] = {(cuuint64_t)dim0, (cuuint64_t)dim1, (cuuint64_t)dim2};
+  cuuint64_t strides[2] = {(cuuint64_t)pitch0 * 2, (cuuint64_t)dim1 * pitch0 * 2};
+  cuuint32_t box[3] = {64, (cuuint32_t)box1, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -355,24 +511,38 @@ bool make_tmap(CUtensorMap* tm, const void* ptr, const Geometry& g, int box_rows
   return r == CUDA_SUCCESS;
 }
 
-template <int D, int BKV>
+template <int D, int BKV, bool QTM, bool VT, int EMU>
 cudaError_t launch_cfg(const Geometry& g, const void* q, const void* k, const void* v, void* out, float* lse,
                        const Workspace& ws, bool rectify, bool text, cudaStream_t st) {
-  using C = Cfg<D, BKV>;
+  using C = Cfg<D, BKV, QTM, VT>;
   CUtensorMap tq, tk, tv;
-  if (!make_tmap(&tq, q, g, 128) || !make_tmap(&tk, k, g, BKV) || !make_tmap(&tv, v, g, BKV))
+  // V^T (K-major B operand of the PV MMA: mixing K- and MN-major B operands
+  // in one MMA stream costs ~35% tensor throughput on sm_100a, measured)
+  if (VT) {
+    dim3 tg((unsigned)((g.T + 63) / 64), (unsigned)(g.d / 64), (unsigned)g.H);
+    transpose_v_kernel<<<tg, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(v), ws.v_t, g.T, vt_pitch(g), g.d);
+  }
+  if (!make_tmap_3d(&tq, q, g.d, g.T, g.H, 128) || !make_tmap_3d(&tk, k, g.d, g.T, g.H, BKV) ||
+      !(VT ? make_tmap_3d(&tv, ws.v_t, g.T, g.d, g.H, D, vt_pitch(g)) : make_tmap_3d(&tv, v, g.d, g.T, g.H, BKV)))
     return cudaErrorInvalidValue;
   TcParams P;
   P.g = g;
   P.ws = ws;
   P.out = static_cast<__nv_bfloat16*>(out);
+  P.q = static_cast<const __nv_bfloat16*>(q);
+  const char* md = getenv("RSA_TC_MODE");
+  P.mode = md ? atoi(md) : 0;
+  const char* sp = getenv("RSA_TC_STAMPS");
+  P.stamps = sp ? atoi(sp) : 0;
+  const char* tc_cta = getenv("RSA_TC_TRACE_CTA");
+  P.trace_cta = tc_cta ? atoi(tc_cta) : 5000;
   P.lse = lse;
   P.rectify = rectify ? 1 : 0;
   P.text_tiles_per_head = (g.Tt + 127) / 128;
   P.n_text_tiles = text ? g.H * P.text_tiles_per_head : 0;
   P.video_tiles_per_head = (g.N * g.B + 127) / 128;
   P.scale_log2 = (float)(1.4426950408889634 / sqrt((double)g.d));
-  auto kern = attn_tc_kernel<D, BKV>;
+  auto kern = attn_tc_kernel<D, BKV, QTM, VT, EMU>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   if (e != cudaSuccess) return e;
   const int64_t tiles = P.n_text_tiles + g.H * P.video_tiles_per_head;
@@ -389,11 +559,28 @@ bool tc_supported(const Geometry& g) {
 
 cudaError_t launch_attn_tc(const Geometry& g, const void* q, const void* k, const void* v, void* out, float* lse,
                            const Workspace& ws, bool rectify, bool text, cudaStream_t st, int* launches) {
-  ++*launches;
-  if (g.d == 128 && g.B == 128) return launch_cfg<128, 128>(g, q, k, v, out, lse, ws, rectify, text, st);
-  if (g.d == 128 && g.B == 64) return launch_cfg<128, 64>(g, q, k, v, out, lse, ws, rectify, text, st);
-  if (g.d == 64 && g.B == 128) return launch_cfg<64, 128>(g, q, k, v, out, lse, ws, rectify, text, st);
-  return launch_cfg<64, 64>(g, q, k, v, out, lse, ws, rectify, text, st);
+  static const bool vt_on = [] { const char* e = getenv("RSA_TC_VT"); return e && atoi(e) != 0; }();
+  *launches += vt_on ? 2 : 1;   // (V transpose) + attention
+  // Variant knobs (profiling): RSA_TC_QTMEM=1 keeps Q in TMEM (2 S buffers);
+  // RSA_TC_VT=0 streams V as an MN-major operand instead of V^T.
+  static const int qtm = [] { const char* e = getenv("RSA_TC_QTMEM"); return e ? atoi(e) : 1; }();
+  static const int vt = [] { const char* e = getenv("RSA_TC_VT"); return e ? atoi(e) : 0; }();
+  const int sel = (qtm ? 2 : 0) + (vt ? 1 : 0);
+#define RSA_TC_CASE(DD, BB)                                                                          \
+  if (g.d == DD && g.B == BB) {                                                                      \
+    switch (sel) {                                                                                   \
+      case 0: return launch_cfg<DD, BB, false, false, 0>(g, q, k, v, out, lse, ws, rectify, text, st); \
+      case 2: return launch_cfg<DD, BB, true, false, 0>(g, q, k, v, out, lse, ws, rectify, text, st);  \
+      case 3: return launch_cfg<DD, BB, true, true, 0>(g, q, k, v, out, lse, ws, rectify, text, st);   \
+      default: return launch_cfg<DD, BB, false, true, 0>(g, q, k, v, out, lse, ws, rectify, text, st); \
+    }                                                                                                \
+  }
+  RSA_TC_CASE(128, 128)
+  RSA_TC_CASE(128, 64)
+  RSA_TC_CASE(64, 128)
+  RSA_TC_CASE(64, 64)
+#undef RSA_TC_CASE
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace rsa

@@ -103,6 +103,7 @@ void layout_of(const rsa::Geometry& g, rsa_workspace_layout* L) {
   L->kv_list = take(H * N * M * 4);
   L->tile_count = take(H * TT * 4);
   L->tile_list = take(H * TT * M * 4);
+  L->v_t = take(g.dtype == RSA_BF16 ? H * (size_t)((g.T + 7) / 8 * 8) * d * 2 : 0);   // pitch % 8 == 0
   L->total = off;
 }
 
@@ -127,6 +128,7 @@ rsa::Workspace bind(const rsa::Geometry& g, void* base) {
   w.kv_list = reinterpret_cast<int32_t*>(b + L.kv_list);
   w.tile_count = reinterpret_cast<int32_t*>(b + L.tile_count);
   w.tile_list = reinterpret_cast<int32_t*>(b + L.tile_list);
+  w.v_t = reinterpret_cast<__nv_bfloat16*>(b + L.v_t);
   return w;
 }
 

@@ -8,10 +8,12 @@
 //
 // Layout: one CTA per (block, segment, head); 256 threads stream the block's
 // rows with 128-bit non-allocating loads (8 bf16 / 4 f32 / 2 f64 per load),
-// each thread owning a column chunk and a row phase.  Partial column sums are
-// kept as (hi, lo) TwoSum pairs and merged in a fixed order, so the result is
-// the exactly rounded sum (bit-identical to fsum for bf16/f32 data, whose
-// partial sums are exact in fp64 anyway) and independent of launch geometry.
+// each thread owning a column chunk and a row phase.  For bf16/f32 data the
+// sums are plain fp64 adds, proven exact per block from its magnitude range
+// (see pass 1 below); otherwise (f64 data, or a block spanning too many
+// binades) partial sums are (hi, lo) TwoSum pairs.  Either way the merged
+// result is the exactly rounded sum, i.e. bit-identical to math.fsum, and
+// independent of launch geometry.
 #include "rsa_internal.cuh"
 
 namespace rsa {
@@ -23,6 +25,21 @@ __device__ __forceinline__ void two_sum(double a, double b, double& s, double& e
   s = a + b;
   double bb = s - a;
   e = (a - (s - bb)) + (b - bb);
+}
+
+template <typename T, int VEC>
+__device__ __forceinline__ void load_vec_f32(const T* p, float (&out)[VEC]) {
+  if constexpr (VEC * sizeof(T) == 16) {
+    uint4 raw;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(raw.x), "=r"(raw.y), "=r"(raw.z), "=r"(raw.w) : "l"(p));
+    const T* v = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) out[i] = to_f32(v[i]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) out[i] = to_f32(p[i]);
+  }
 }
 
 template <typename T, int VEC>
@@ -66,63 +83,125 @@ pool_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restric
   const bool text_k = (seg == 1) && (blk >= g.N);
   double* raw_out = text_k ? ws.k_cat + (h * g.n_cols + g.N + (row0 - g.Tv)) * d : nullptr;
 
-  double hi[VEC], lo[VEC];
+  // Pass 1 (bf16 / f32 data): plain fp64 sums plus the block's magnitude
+  // range.  Every value is a multiple of 2^(e_min - p + 1) (p significant
+  // bits), so all partial sums are exact in fp64 while
+  //   e_max - e_min + p + ceil(log2(len)) < 53;
+  // then the plain sums ARE the exactly rounded sums.  Otherwise (or for f64
+  // data) pass 2 recomputes the block with TwoSum (hi, lo) pairs.
+  constexpr bool kTryPlain = sizeof(T) < 8;
+  constexpr int kMant = sizeof(T) == 2 ? 8 : 24;
+  __shared__ float s_amax[kThreads / 32], s_amin[kThreads / 32];
+  __shared__ int s_exact;
+  bool exact = false;
+  if constexpr (kTryPlain) {
+    double acc[VEC];
+    float amax = 0.f, amin = INFINITY;
 #pragma unroll
-  for (int i = 0; i < VEC; ++i) { hi[i] = 0.0; lo[i] = 0.0; }
-  if (rg < rg_count) {
-    int64_t r = rg;
-    // 4 independent loads in flight per thread
-    for (; r + 3 * rg_count < len; r += 4 * rg_count) {
-      double x[4][VEC];
+    for (int i = 0; i < VEC; ++i) acc[i] = 0.0;
+    if (rg < rg_count) {
+      int64_t r = rg;
+      for (; r + 7 * rg_count < len; r += 8 * rg_count) {
+        float x[8][VEC];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) load_vec<T, VEC>(src + (r + u * rg_count) * d + c * VEC, x[u]);
+        for (int u = 0; u < 8; ++u) load_vec_f32<T, VEC>(src + (r + u * rg_count) * d + c * VEC, x[u]);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 8; ++u) {
+#pragma unroll
+          for (int i = 0; i < VEC; ++i) {
+            acc[i] += (double)x[u][i];
+            const float ax = fabsf(x[u][i]);
+            amax = fmaxf(amax, ax);
+            amin = fminf(amin, ax > 0.f ? ax : INFINITY);
+          }
+          if (raw_out) {
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) raw_out[(r + u * rg_count) * d + c * VEC + i] = (double)x[u][i];
+          }
+        }
+      }
+      for (; r < len; r += rg_count) {
+        float x[VEC];
+        load_vec_f32<T, VEC>(src + r * d + c * VEC, x);
 #pragma unroll
         for (int i = 0; i < VEC; ++i) {
-          double s, e;
-          two_sum(hi[i], x[u][i], s, e);
-          hi[i] = s;
-          lo[i] += e;
+          acc[i] += (double)x[i];
+          const float ax = fabsf(x[i]);
+          amax = fmaxf(amax, ax);
+          amin = fminf(amin, ax > 0.f ? ax : INFINITY);
         }
         if (raw_out) {
 #pragma unroll
-          for (int i = 0; i < VEC; ++i) raw_out[(r + u * rg_count) * d + c * VEC + i] = x[u][i];
+          for (int i = 0; i < VEC; ++i) raw_out[r * d + c * VEC + i] = (double)x[i];
         }
       }
-    }
-    for (; r < len; r += rg_count) {
-      double x[VEC];
-      load_vec<T, VEC>(src + r * d + c * VEC, x);
 #pragma unroll
       for (int i = 0; i < VEC; ++i) {
-        double s, e;
-        two_sum(hi[i], x[i], s, e);
-        hi[i] = s;
-        lo[i] += e;
-      }
-      if (raw_out) {
-#pragma unroll
-        for (int i = 0; i < VEC; ++i) raw_out[r * d + c * VEC + i] = x[i];
+        s_hi[rg * d + i * tpr + c] = acc[i];   // column-interleaved: conflict-free
       }
     }
 #pragma unroll
-    for (int i = 0; i < VEC; ++i) {
-      s_hi[rg * d + c * VEC + i] = hi[i];
-      s_lo[rg * d + c * VEC + i] = lo[i];
+    for (int o = 16; o > 0; o >>= 1) {
+      amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      amin = fminf(amin, __shfl_xor_sync(0xffffffffu, amin, o));
+    }
+    if (t % 32 == 0) { s_amax[t / 32] = amax; s_amin[t / 32] = amin; }
+    __syncthreads();
+    if (t == 0) {
+      float mx = 0.f, mn = INFINITY;
+      for (int w = 0; w < kThreads / 32; ++w) { mx = fmaxf(mx, s_amax[w]); mn = fminf(mn, s_amin[w]); }
+      int lg = 0;
+      while ((int64_t(1) << lg) < len) ++lg;
+      s_exact = (mn == INFINITY) || (ilogbf(mx) - ilogbf(mn) + kMant + lg < 53);
+    }
+    __syncthreads();
+    exact = s_exact != 0;
+  }
+  if (!exact) {
+    double hi[VEC], lo[VEC];
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) { hi[i] = 0.0; lo[i] = 0.0; }
+    if (rg < rg_count) {
+      for (int64_t r = rg; r < len; r += rg_count) {
+        double x[VEC];
+        load_vec<T, VEC>(src + r * d + c * VEC, x);
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) {
+          double sm, e;
+          two_sum(hi[i], x[i], sm, e);
+          hi[i] = sm;
+          lo[i] += e;
+        }
+        if (raw_out && !kTryPlain) {
+#pragma unroll
+          for (int i = 0; i < VEC; ++i) raw_out[r * d + c * VEC + i] = x[i];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) {
+        s_hi[rg * d + i * tpr + c] = hi[i];
+        s_lo[rg * d + i * tpr + c] = lo[i];
+      }
     }
   }
   __syncthreads();
 
   for (int64_t col = t; col < d; col += kThreads) {
-    double S = 0.0, E = 0.0;
-    for (int p = 0; p < rg_count; ++p) {
-      double s, e;
-      two_sum(S, s_hi[p * d + col], s, e);
-      S = s;
-      E += e + s_lo[p * d + col];
+    const int64_t slot = (col % VEC) * tpr + col / VEC;
+    double sum;
+    if (exact) {
+      sum = 0.0;   // exact partial sums: plain adds stay exact (same bound)
+      for (int p = 0; p < rg_count; ++p) sum += s_hi[p * d + slot];
+    } else {
+      double S = 0.0, E = 0.0;
+      for (int p = 0; p < rg_count; ++p) {
+        double s, e;
+        two_sum(S, s_hi[p * d + slot], s, e);
+        S = s;
+        E += e + s_lo[p * d + slot];
+      }
+      sum = S + E;                            // exactly rounded block sum
     }
-    const double sum = S + E;                 // exactly rounded block sum
     const double flen = (double)len;
     const double mean = sum / flen;           // core.py:172 fsum(...) / length
     const double deficit = sum - flen * mean; // masks.py:166 / masks.py:171

@@ -27,6 +27,7 @@ struct Workspace {
   int32_t* kv_list;
   int32_t* tile_count;
   int32_t* tile_list;
+  __nv_bfloat16* v_t;   // [H][d][T] transposed V (tcgen05 path)
   int32_t* status;
 };
 

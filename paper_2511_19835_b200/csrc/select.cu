@@ -170,6 +170,26 @@ __device__ __forceinline__ bool before(double va, int ia, double vb, int ib) {
   return va > vb || (va == vb && ia < ib);
 }
 
+// in-place bitonic sort of n (power of two) (value, index) pairs in shared
+// memory into (value desc, index asc) order
+__device__ void bitonic_sort(double* sv, int* si, int n) {
+  for (int kk = 2; kk <= n; kk <<= 1) {
+    for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+      for (int i = threadIdx.x; i < n; i += RT) {
+        const int ixj = i ^ jj;
+        if (ixj > i) {
+          const bool up = (i & kk) == 0;
+          const double va = sv[i], vb = sv[ixj];
+          const int ia = si[i], ib = si[ixj];
+          const bool swap = up ? before(vb, ib, va, ia) : before(va, ia, vb, ib);
+          if (swap) { sv[i] = vb; sv[ixj] = va; si[i] = ib; si[ixj] = ia; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
 __global__ void __launch_bounds__(RT) select_rows_kernel(SelectParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Geometry& g = P.g;
@@ -185,6 +205,8 @@ __global__ void __launch_bounds__(RT) select_rows_kernel(SelectParams P) {
   __shared__ double red[RT / 32];
   __shared__ int scan_tmp[RT];
   __shared__ int sh_count;
+  __shared__ unsigned hist[256];
+  __shared__ int sh_digit, sh_rem;
 
   const double* srow = ws.scores + (h * N + n) * n_cols;
 
@@ -229,41 +251,111 @@ __global__ void __launch_bounds__(RT) select_rows_kernel(SelectParams P) {
   if (full) {
     for (int64_t m = threadIdx.x; m < M; m += RT) bits[m] = BIT_MASK | BIT_IMPORTANCE;
   } else {
-    for (int i = threadIdx.x; i < P.p2; i += RT) {
-      sv[i] = i < M ? ap[i] : -1.0;
-      si[i] = i < M ? i : 0x7fffffff;
-    }
-    __syncthreads();
-    for (int kk = 2; kk <= P.p2; kk <<= 1) {
-      for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-        for (int i = threadIdx.x; i < P.p2; i += RT) {
-          const int ixj = i ^ jj;
-          if (ixj > i) {
-            const bool up = (i & kk) == 0;
-            const double va = sv[i], vb = sv[ixj];
-            const int ia = si[i], ib = si[ixj];
-            const bool swap = up ? before(vb, ib, va, ia) : before(va, ia, vb, ib);
-            if (swap) { sv[i] = vb; sv[ixj] = va; si[i] = ib; si[ixj] = ia; }
+    // Exact top-K (K = ceil(f*M), masks.py:100) by MSB-first radix select on
+    // the fp64 bit patterns (a_pool >= 0, so unsigned order == value order),
+    // ties resolved by ascending block index -- the set numpy's stable
+    // argsort(-a) puts first.  The cumulative-weight rule (masks.py:101-103)
+    // can only enlarge the count beyond K when the sequential cumsum of the
+    // sorted top-K stays below p; only then is the full sort needed.
+    const int64_t K = P.k_floor < M ? P.k_floor : M;
+    uint64_t prefix = 0, pmask = 0;
+    int remaining = (int)K;
+    for (int shift = 56; shift >= 0; shift -= 8) {
+      for (int i = threadIdx.x; i < 256; i += RT) hist[i] = 0u;
+      __syncthreads();
+      for (int64_t m = threadIdx.x; m < M; m += RT) {
+        const uint64_t key = (uint64_t)__double_as_longlong(ap[m]);
+        if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 0xFF], 1u);
+      }
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        unsigned c[8], tot = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) { c[i] = hist[255 - 8 * lane - i]; tot += c[i]; }
+        unsigned incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const unsigned excl = incl - tot;
+        if (excl < (unsigned)remaining && incl >= (unsigned)remaining) {
+          unsigned run = excl;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            if (run + c[i] >= (unsigned)remaining) { sh_digit = 255 - 8 * lane - i; sh_rem = remaining - (int)run; break; }
+            run += c[i];
           }
         }
-        __syncthreads();
+      }
+      __syncthreads();
+      prefix |= (uint64_t)sh_digit << shift;
+      pmask |= (uint64_t)0xFF << shift;
+      remaining = sh_rem;
+    }
+    {
+      // keys > v* are in; the first `remaining` keys == v* (ascending index) too
+      const int64_t chunk = (M + RT - 1) / RT;
+      const int64_t lo = threadIdx.x * chunk, hi = min(lo + chunk, M);
+      int eq = 0;
+      for (int64_t m = lo; m < hi; ++m) eq += (uint64_t)__double_as_longlong(ap[m]) == prefix;
+      int tot_eq;
+      int rank = block_excl_scan(eq, scan_tmp, &tot_eq);
+      for (int64_t m = lo; m < hi; ++m) {
+        const uint64_t key = (uint64_t)__double_as_longlong(ap[m]);
+        if (key > prefix || (key == prefix && rank++ < remaining)) bits[m] = BIT_IMPORTANCE;
       }
     }
-    if (threadIdx.x == 0) {
-      // sequential cumsum in sorted order, exactly as numpy.cumsum (masks.py:99-102)
-      int64_t first_p = M;
-      double cum = 0.0;
-      for (int64_t i = 0; i < M; ++i) {
-        cum += sv[i];
-        if (cum >= P.p) { first_p = i + 1; break; }
+    __syncthreads();
+    bool need_full_sort = false;
+    if (P.p > 0.0) {
+      // sequential cumsum of the top-K in sorted order (masks.py:99): gather, sort, sum
+      int kp2 = 1;
+      while (kp2 < K) kp2 <<= 1;
+      const int64_t chunk = (M + RT - 1) / RT;
+      const int64_t lo = threadIdx.x * chunk, hi = min(lo + chunk, M);
+      int mine = 0;
+      for (int64_t m = lo; m < hi; ++m) mine += bits[m] & BIT_IMPORTANCE ? 1 : 0;
+      int tot_k;
+      int off = block_excl_scan(mine, scan_tmp, &tot_k);
+      for (int64_t m = lo; m < hi; ++m)
+        if (bits[m] & BIT_IMPORTANCE) { sv[off] = ap[m]; si[off] = (int)m; ++off; }
+      for (int i = tot_k + threadIdx.x; i < kp2; i += RT) { sv[i] = -1.0; si[i] = 0x7fffffff; }
+      __syncthreads();
+      bitonic_sort(sv, si, kp2);
+      if (threadIdx.x == 0) {
+        double cum = 0.0;
+        for (int64_t i = 0; i < K; ++i) cum += sv[i];
+        sh_count = cum >= P.p ? 0 : 1;
       }
-      int64_t count = first_p > P.k_floor ? first_p : P.k_floor;
-      count = count < 1 ? 1 : (count > M ? M : count);
-      sh_count = (int)count;
+      __syncthreads();
+      need_full_sort = sh_count != 0;
     }
-    __syncthreads();
-    for (int i = threadIdx.x; i < sh_count; i += RT) bits[si[i]] = BIT_IMPORTANCE;
-    __syncthreads();
+    if (need_full_sort) {
+      for (int i = threadIdx.x; i < P.p2; i += RT) {
+        sv[i] = i < M ? ap[i] : -1.0;
+        si[i] = i < M ? i : 0x7fffffff;
+      }
+      for (int64_t m = threadIdx.x; m < M; m += RT) bits[m] = 0;
+      __syncthreads();
+      bitonic_sort(sv, si, P.p2);
+      if (threadIdx.x == 0) {
+        // sequential cumsum in sorted order, exactly as numpy.cumsum (masks.py:99-102)
+        int64_t first_p = M;
+        double cum = 0.0;
+        for (int64_t i = 0; i < M; ++i) {
+          cum += sv[i];
+          if (cum >= P.p) { first_p = i + 1; break; }
+        }
+        int64_t count = first_p > P.k_floor ? first_p : P.k_floor;
+        count = count < 1 ? 1 : (count > M ? M : count);
+        sh_count = (int)count;
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < sh_count; i += RT) bits[si[i]] = BIT_IMPORTANCE;
+      __syncthreads();
+    }
     for (int64_t m = threadIdx.x; m < M; m += RT) {
       uint8_t b = bits[m];
       const int64_t dist = m > n ? m - n : n - m;

@@ -171,6 +171,21 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// 2^x for x <= 0 on the FMA/ALU pipes (FA4-style MUFU offload): round-to-
+// nearest split x = n + f (f in [-0.5, 0.5]) with the 1.5*2^23 magic constant,
+// degree-3 polynomial for 2^f (max rel. error ~1e-4, far below bf16's 2^-8),
+// exponent inserted with an integer add.  x = -inf / x < -127 gives +0.
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -127.f);
+  const float t = x + 12582912.f;
+  const float n = t - 12582912.f;
+  const float f = x - n;
+  float p = fmaf(0.05550411f, f, 0.24022652f);
+  p = fmaf(p, f, 0.69314718f);
+  p = fmaf(p, f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 // pack (lo, hi) into bf16x2 with lo in the low half
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   uint32_t r;

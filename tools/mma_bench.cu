@@ -1,0 +1,119 @@
+// Microbenchmark: cycles per tcgen05.mma (kind::f16, M=128, K=16) for SS / TS
+// operand sources and N = 64 / 128 / 256, one CTA per SM.  Build:
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 tools/mma_bench.cu -o tools/mma_bench
+#include <cstdio>
+#include <cuda_runtime.h>
+#include "../paper_2511_19835_b200/csrc/tc_ptx.cuh"
+
+using namespace rsa::ptx;
+
+template <int N, bool TS, int CHAINS, int COMMIT_EVERY = 0, int MN = 0>
+__global__ void __launch_bounds__(128, 1) bench(long long* out, int iters) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint32_t slot;
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t dummy[4];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x / 32;
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); for (int i = 0; i < 4; ++i) mbar_init(dummy + i, 1); fence_barrier_init(); }
+  if (warp == 0) tmem_alloc<512>(&slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  long long t0 = 0, t1 = 0;
+  if (threadIdx.x == 32) {
+    const uint32_t a_addr = smem_u32(base);
+    const uint32_t b_addr = smem_u32(base + 16384);
+    constexpr uint32_t idesc = idesc_bf16(128, N, MN == 1);
+    constexpr uint32_t idesc_k = idesc_bf16(128, N, false);
+    // warm-up
+    for (int i = 0; i < 64; ++i) {
+      const uint64_t b = sw128_desc(b_addr + (i % 4) * 32, 16, 1024);
+      if (TS) mma_ts(tmem, tmem + 384 + (i % 8) * 8, b, idesc, 1);
+      else mma_ss(tmem, sw128_desc(a_addr + (i % 4) * 32, 16, 1024), b, idesc, 1);
+    }
+    tc_commit(&bar);
+    mbar_wait(&bar, 0);
+    t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+      // MN == 1: B is MN-major (V-style: LBO = panel stride, K step = 16 rows = 2048 B);
+      // MN == 2: alternate 8 K-major (S-style) and 8 MN-major (PV-style) MMAs
+      // MN == 3: K-major only, alternating accumulators every 8; MN == 4: MN-major only, alternating;
+      // MN == 5: alternating majorness, same accumulator and same A
+      const bool mn = MN == 1 || MN == 4 || ((MN == 2 || MN == 5) && ((i / 8) & 1));
+      if (MN >= 3) {
+        const uint64_t bb = mn ? sw128_desc(b_addr + (i % 8) * 2048, 16384, 1024) : sw128_desc(b_addr + (i % 4) * 32, 16, 1024);
+        const uint32_t acc = (MN == 5) ? tmem : tmem + (((i / 8) & 1) ? 256u : 0u);
+        mma_ts(acc, tmem + 384 + (i % 8) * 8, bb, mn ? idesc_bf16(128, N, true) : idesc_k, 1);
+        continue;
+      }
+      const uint64_t b = mn ? sw128_desc(b_addr + (i % 8) * 2048, 16384, 1024)
+                            : sw128_desc(b_addr + (i % 4) * 32, 16, 1024);
+      const uint32_t d = tmem + (CHAINS > 1 ? (uint32_t)((i % CHAINS) * N) : 0u);
+      if (MN == 2) { mma_ts(d, tmem + 384 + (i % 8) * 8, b, mn ? idesc_bf16(128, N, true) : idesc_k, 1); continue; }
+      if (TS) mma_ts(d, tmem + 384 + (i % 8) * 8, b, idesc, 1);
+      else mma_ss(d, sw128_desc(a_addr + (i % 4) * 32, 16, 1024), b, idesc, 1);
+      if (COMMIT_EVERY && (i % COMMIT_EVERY) == COMMIT_EVERY - 1) tc_commit(dummy + ((i / COMMIT_EVERY) & 3));
+    }
+    tc_commit(&bar);
+    mbar_wait(&bar, 1);
+    t1 = clock64();
+    out[blockIdx.x] = t1 - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) { tc_fence_after(); tmem_dealloc<512>(tmem); }
+}
+
+template <int N, bool TS, int CHAINS, int COMMIT_EVERY = 0, int MN = 0>
+void run(const char* name, int sms) {
+  long long* d;
+  cudaMalloc(&d, sms * sizeof(long long));
+  auto k = bench<N, TS, CHAINS, COMMIT_EVERY, MN>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  cudaMemset(d, 0, sms * sizeof(long long));
+  const int iters = 4096;
+  k<<<sms, 128, 100 * 1024>>>(d, iters);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  k<<<sms, 128, 100 * 1024>>>(d, iters);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  long long h[200];
+  cudaMemcpy(h, d, sms * sizeof(long long), cudaMemcpyDeviceToHost);
+  double avg = 0;
+  for (int i = 0; i < sms; ++i) avg += h[i];
+  avg /= sms;
+  const double flops = 2.0 * 128 * N * 16 * iters * sms;
+  printf("%-28s cycles/MMA %7.1f  (ideal %5.1f)  %.0f TFLOP/s over %d SMs  err=%s\n", name, avg / iters,
+         128.0 * N / 256.0, flops / (ms * 1e-3) / 1e12, sms, cudaGetErrorString(cudaGetLastError()));
+  cudaFree(d);
+}
+
+int main() {
+  int sms = 148;
+  run<128, false, 1>("SS N=128", sms);
+  run<128, true, 1>("TS N=128", sms);
+  run<256, false, 1>("SS N=256", sms);
+  run<256, true, 1>("TS N=256", sms);
+  run<64, false, 1>("SS N=64", sms);
+  run<128, false, 2>("SS N=128 2 accumulators", sms);
+  run<128, true, 2>("TS N=128 2 accumulators", sms);
+  run<128, false, 1>("SS N=128 (1 SM)", 1);
+  run<128, false, 1, 8>("SS N=128 commit/8", sms);
+  run<128, true, 1, 8>("TS N=128 commit/8", sms);
+  run<128, false, 1, 16>("SS N=128 commit/16", sms);
+  run<128, false, 1, 4>("SS N=128 commit/4", sms);
+  run<128, false, 1, 0, 1>("SS N=128 B MN-major", sms);
+  run<128, true, 1, 0, 1>("TS N=128 B MN-major", sms);
+  run<128, true, 1, 0, 2>("TS N=128 S/PV alternating", sms);
+  run<64, true, 1, 0, 1>("TS N=64 B MN-major", sms);
+  run<128, true, 1, 0, 3>("TS K-major, 2 accs alt/8", sms);
+  run<128, true, 1, 0, 4>("TS MN-major, 2 accs alt/8", sms);
+  run<128, true, 1, 0, 5>("TS K/MN alt/8 same acc", sms);
+  return 0;
+}
