@@ -66,6 +66,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-blocks", type=int, default=96)
     ap.add_argument("--profile", action="store_true", help="fewer steps, no side legs (for ncu)")
+    ap.add_argument("--input-layout", choices=["heads", "seq"], default="heads",
+                    help="heads: inputs head-sharded (no collective); seq: video tokens sequence-"
+                         "sharded, Ulysses NCCL all-to-all before/after the pipeline (N>1)")
     return ap.parse_args()
 
 
@@ -303,10 +306,36 @@ def run_ours(args):
         if record:
             ev[3].record(st)
 
+    ulysses = args.input_layout == "seq" and world > 1
+    if ulysses:
+        # every rank holds its T_v/P slice of all heads' video tokens + replicated text
+        from paper_2511_19835_b200.parallel import ulysses_attention
+        qa, ka, va = synth_inputs(torch, cfg, cfg["heads"], 1234, dev)
+        t_v = cfg["t_v"]
+        s_loc = t_v // world
+        sl = slice(rank * s_loc, (rank + 1) * s_loc)
+        uq, uk, uv = (x[None, :, sl].contiguous() for x in (qa, ka, va))
+        tq, tk, tv = (x[None, :, t_v:].contiguous() for x in (qa, ka, va))
+        del qa, ka, va
+
+        def uattn(q_, k_, v_, t_t_):
+            return rsa.rectified_sparse_attention(q_, k_, v_, num_text_tokens=t_t_, block=cfg["block"],
+                                                  top_k_fraction=f, variant=args.variant, kernel=args.kernel,
+                                                  workspace=ws)
+
+        def step(record=False):
+            if record:
+                ev[0].record(st)
+                ev[1].record(st)
+                ev[2].record(st)
+            ulysses_attention(uq, uk, uv, tq, tk, tv, attn_fn=uattn)
+            if record:
+                ev[3].record(st)
+
     for _ in range(args.warmup):
         c0 = nat.last_launch_count()
         step()
-        launches_per_step = nat.last_launch_count() - c0
+        launches_per_step = nat.last_launch_count() - (0 if ulysses else c0)
     nat.check(lib.rsa_check_device_status(_ptr(ws), sptr))
     torch.cuda.synchronize()
 
@@ -417,7 +446,9 @@ def run_ours(args):
         "config": {"workload": cfg["label"], "heads": cfg["heads"], "t_video": cfg["t_v"], "t_text": cfg["t_t"],
                    "head_dim": d, "block": cfg["block"], "top_k_fraction": round(f, 6),
                    "weight_threshold": 0.0, "adjacency_radius": 0, "force_text_blocks": False,
-                   "variant": args.variant, "parallelism": f"head-sharded x{world}",
+                   "variant": args.variant,
+                   "parallelism": (f"Ulysses seq->head all-to-all x{world} (NCCL)" if ulysses
+                                   else f"head-sharded x{world}"),
                    "l2": "inputs 2.2 GB >> 126 MB L2 (no flush needed)" if args.config != "cfg1"
                    else "inputs 6 MB; L2 resident", "kernel": args.kernel},
         "tflops_effective": flops_exec / (ms_step * 1e-3) / 1e12,
