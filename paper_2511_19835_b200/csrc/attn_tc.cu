@@ -66,10 +66,14 @@ struct TcParams {
   __nv_bfloat16* out;
   const __nv_bfloat16* q;
   float* lse;
+  float* text_part;   // [H][text tiles][chunks][128][D] unnormalised partial O
+  float2* text_ml;    // [H][text tiles][chunks][128] (row max log2, row sum)
   int rectify;
-  int64_t n_text_tiles;
-  int64_t text_tiles_per_head;
+  int64_t text_tiles_per_head;   // 128-row text query tiles per head (0: no text queries)
+  int64_t text_chunks;           // kv-block chunks per text tile (split-K)
+  int64_t chunk_blocks;          // kv blocks per chunk
   int64_t video_tiles_per_head;
+  int64_t tiles_per_head;        // text_tiles_per_head * text_chunks + video_tiles_per_head
   float scale_log2;  // log2(e) / sqrt(d)
   int trace_cta;     // CTA traced per step when stamps == 2
   int stamps;        // RSA_TC_STAMPS=1: per-CTA globaltimer stamps into `lse` (profiling)
@@ -116,21 +120,26 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     tstamp[7] = smid;
   }
 
-  // ---- tile decode (LPT order: text tiles first) ----
+  // ---- tile decode: head-major, each head's text chunks first, then its
+  // video tiles, so the K/V blocks of ~one head are in flight at a time (L2).
+  // A text tile walks every kv block; it is split into `text_chunks` chunks of
+  // `chunk_blocks` blocks whose partial (O, m, l) text_combine_kernel merges.
   const int64_t bid = blockIdx.x;
-  const bool text = bid < P.n_text_tiles;
-  int64_t h, q_row0, rows_valid, count;
+  const int64_t h = bid / P.tiles_per_head;
+  const int64_t r_in = bid % P.tiles_per_head;
+  const int64_t n_text_ct = P.text_tiles_per_head * P.text_chunks;
+  const bool text = r_in < n_text_ct;
+  int64_t q_row0, rows_valid, count, m_first = 0, part = 0;
   const int32_t* list = nullptr;
   if (text) {
-    h = bid / P.text_tiles_per_head;
-    const int64_t t = bid % P.text_tiles_per_head;
+    const int64_t t = r_in / P.text_chunks, c = r_in % P.text_chunks;
     q_row0 = g.Tv + t * 128;
     rows_valid = min((int64_t)128, g.Tt - t * 128);
-    count = g.M;
+    m_first = c * P.chunk_blocks;
+    count = min(g.M, m_first + P.chunk_blocks) - m_first;
+    part = (h * P.text_tiles_per_head + t) * P.text_chunks + c;
   } else {
-    const int64_t b = bid - P.n_text_tiles;
-    h = b / P.video_tiles_per_head;
-    const int64_t t = b % P.video_tiles_per_head;
+    const int64_t t = r_in - n_text_ct;
     q_row0 = t * 128;
     rows_valid = min((int64_t)128, g.Tv - q_row0);
     count = P.ws.tile_count[h * P.video_tiles_per_head + t];
@@ -170,10 +179,11 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           ptx::tma_load_3d(q_s + p * C::Q_PANEL, &tm_q, q_full, 64 * p, (int)q_row0, (int)h);
       }
       int it = 0;
+      const uint64_t keep = ptx::policy_evict_last();   // K/V blocks are re-read by many tiles of the head
       auto load = [&](int64_t j, bool is_v) {
         const int s = it % C::NST;
         const uint32_t ph = (it / C::NST) & 1;
-        const int64_t m = list ? (list[j] & 0xFFFFFF) : j;
+        const int64_t m = list ? (list[j] & 0xFFFFFF) : m_first + j;
         ptx::mbar_wait(kv_empty + s, ph ^ 1);
         if (trace && j < 64) trace[j * 8 + (is_v ? 7 : 6)] = clock64();
         ptx::mbar_expect_tx(kv_full + s, C::STAGE);
@@ -181,11 +191,11 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         const int panels = (is_v && VT) ? BKV / 64 : C::PANELS;
         for (int p = 0; p < panels; ++p)
           if (is_v && VT)   // V^T: box (64 keys, D dims) per 64-key panel
-            ptx::tma_load_3d(dst + p * C::VT_PANEL, &tm_v, kv_full + s, (int)(m * g.B) + 64 * p, 0, (int)h);
+            ptx::tma_load_3d_hint(dst + p * C::VT_PANEL, &tm_v, kv_full + s, (int)(m * g.B) + 64 * p, 0, (int)h, keep);
           else if (is_v)    // V: box (64 dims, B keys) per 64-dim panel
-            ptx::tma_load_3d(dst + p * C::KV_PANEL, &tm_v, kv_full + s, 64 * p, (int)(m * g.B), (int)h);
+            ptx::tma_load_3d_hint(dst + p * C::KV_PANEL, &tm_v, kv_full + s, 64 * p, (int)(m * g.B), (int)h, keep);
           else
-            ptx::tma_load_3d(dst + p * C::KV_PANEL, &tm_k, kv_full + s, 64 * p, (int)(m * g.B), (int)h);
+            ptx::tma_load_3d_hint(dst + p * C::KV_PANEL, &tm_k, kv_full + s, 64 * p, (int)(m * g.B), (int)h, keep);
         ++it;
       };
       for (int64_t j = 0; j <= count; ++j) {
@@ -195,7 +205,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
-    if (lane == 0 && count > 0 && P.mode == 6) {
+    if (P.mode == 6 || P.mode == 2) {
+      if (lane == 0 && count > 0 && P.mode == 6) {
       // diagnostic: softmax alone -- hand out S buffers without any MMA
       for (int64_t j = 0; j < count; ++j) {
         if (j >= 1) {
@@ -206,63 +217,79 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       }
       ptx::mbar_wait(p_full + ((count - 1) % C::NS), (uint32_t)(((count - 1) / C::NS) & 1));
       ptx::tc_commit(pv_done);
-    } else if (lane == 0 && count > 0 && P.mode == 2) {
+      } else if (lane == 0 && count > 0) {
       // diagnostic: consume the K/V stream without any MMA (TMA rate only)
       for (int it = 0; it < 2 * count; ++it) {
         ptx::mbar_wait(kv_full + it % C::NST, (it / C::NST) & 1);
         ptx::mbar_arrive(kv_empty + it % C::NST);
       }
-    } else if (lane == 0 && count > 0) {
+      }
+    } else if (count > 0) {
+      // The whole warp runs the issue loop (converged, warp-uniform
+      // descriptors in uniform registers); one elected lane issues each
+      // tcgen05.mma / commit.  Lane-0-only code made the compiler wrap every
+      // UTCHMMA in an ELECT/R2UR.BROADCAST waterfall (~15 instr, profiles/r01a).
       ptx::mbar_wait(q_full, 0);
       ptx::tc_fence_after();
-      if (tstamp) tstamp[2] = gtimer();
-      const uint32_t q_addr = ptx::smem_u32(q_s);
-      const uint32_t kv_addr = ptx::smem_u32(kv_s);
-      int it = 0;
+      if (tstamp && lane == 0) tstamp[2] = gtimer();
+      const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+      const uint32_t kv_addr = __shfl_sync(0xffffffffu, ptx::smem_u32(kv_s), 0);
+      const uint32_t q_addr = __shfl_sync(0xffffffffu, ptx::smem_u32(q_s), 0);
+      int s_kv = 0;
+      uint32_t ph_kv = 0;
+      auto advance = [&]() {
+        if (++s_kv == C::NST) { s_kv = 0; ph_kv ^= 1u; }
+      };
       for (int64_t j = 0; j <= count; ++j) {
         if (j < count) {
-          const int s = it % C::NST;
-          if (P.mode != 3) ptx::mbar_wait(kv_full + s, (it / C::NST) & 1);
-          if (trace && j < 64) trace[j * 8 + 0] = clock64();
+          if (P.mode != 3) ptx::mbar_wait(kv_full + s_kv, ph_kv);
+          if (trace && lane == 0 && j < 64) trace[j * 8 + 0] = clock64();
           ptx::tc_fence_after();
-          const uint32_t d_tmem = tmem + (uint32_t)((j % C::NS) * BKV);
+          const uint32_t d_tmem = tm + (uint32_t)((j % C::NS) * BKV);
+          const uint32_t kb = kv_addr + (uint32_t)(s_kv * C::STAGE);
+          if (ptx::elect_one()) {
 #pragma unroll
-          for (int k = 0; k < D / 16; ++k) {
-            const uint32_t off = (uint32_t)((k % 4) * 32);   // 16 bf16 = 32 B inside the 128 B row
-            const uint64_t b = ptx::sw128_desc(kv_addr + s * C::STAGE + (k / 4) * C::KV_PANEL + off, 16, 1024);
-            if (QTM) {
-              ptx::mma_ts(d_tmem, tmem + C::Q_COL + k * 8, b, C::IDESC_S, k > 0);
-            } else {
-              const uint64_t a = ptx::sw128_desc(q_addr + (k / 4) * C::Q_PANEL + off, 16, 1024);
-              ptx::mma_ss(d_tmem, a, b, C::IDESC_S, k > 0);
+            for (int k = 0; k < D / 16; ++k) {
+              const uint32_t off = (uint32_t)((k % 4) * 32);   // 16 bf16 = 32 B inside the 128 B row
+              const uint64_t b = ptx::sw128_desc(kb + (k / 4) * C::KV_PANEL + off, 16, 1024);
+              if (QTM) {
+                ptx::mma_ts(d_tmem, tm + C::Q_COL + k * 8, b, C::IDESC_S, k > 0);
+              } else {
+                const uint64_t a = ptx::sw128_desc(q_addr + (k / 4) * C::Q_PANEL + off, 16, 1024);
+                ptx::mma_ss(d_tmem, a, b, C::IDESC_S, k > 0);
+              }
             }
+            ptx::tc_commit(kv_empty + s_kv);
+            ptx::tc_commit(s_full + (j % C::NS));
           }
-          ptx::tc_commit(kv_empty + s);
-          ptx::tc_commit(s_full + (j % C::NS));
-          ++it;
+          __syncwarp();
+          advance();
         }
         if (j >= 1) {
           const int64_t jj = j - 1;
           if (P.mode < 3) ptx::mbar_wait(p_full + (jj % C::NS), (uint32_t)((jj / C::NS) & 1));
-          if (trace && jj < 64) trace[jj * 8 + 1] = clock64();
-          const int s = it % C::NST;
-          if (P.mode != 3) ptx::mbar_wait(kv_full + s, (it / C::NST) & 1);
-          if (trace && jj < 64) trace[jj * 8 + 2] = clock64();
+          if (trace && lane == 0 && jj < 64) trace[jj * 8 + 1] = clock64();
+          if (P.mode != 3) ptx::mbar_wait(kv_full + s_kv, ph_kv);
+          if (trace && lane == 0 && jj < 64) trace[jj * 8 + 2] = clock64();
           ptx::tc_fence_after();
-          const uint32_t a_tmem = tmem + (uint32_t)((jj % C::NS) * BKV);
+          const uint32_t a_tmem = tm + (uint32_t)((jj % C::NS) * BKV);
+          const uint32_t vb = kv_addr + (uint32_t)(s_kv * C::STAGE);
+          if (ptx::elect_one()) {
 #pragma unroll
-          for (int k = 0; k < BKV / 16; ++k) {
-            const uint64_t b = VT ? ptx::sw128_desc(kv_addr + s * C::STAGE + (k / 4) * C::VT_PANEL + (k % 4) * 32, 16, 1024)
-                                  : ptx::sw128_desc(kv_addr + s * C::STAGE + k * 2048, C::KV_PANEL, 1024);
-            ptx::mma_ts(tmem + C::O_COL, a_tmem + k * 8, b, C::IDESC_O, (jj > 0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < BKV / 16; ++k) {
+              const uint64_t b = VT ? ptx::sw128_desc(vb + (k / 4) * C::VT_PANEL + (k % 4) * 32, 16, 1024)
+                                    : ptx::sw128_desc(vb + k * 2048, C::KV_PANEL, 1024);
+              ptx::mma_ts(tm + C::O_COL, a_tmem + k * 8, b, C::IDESC_O, (jj > 0 || k > 0) ? 1u : 0u);
+            }
+            ptx::tc_commit(kv_empty + s_kv);
+            ptx::tc_commit(pv_done);
           }
-          ptx::tc_commit(kv_empty + s);
-          ptx::tc_commit(pv_done);
-          ++it;
+          __syncwarp();
+          advance();
         }
       }
       if (P.mode >= 3 && P.mode <= 4) ptx::mbar_wait(pv_done, (uint32_t)((count - 1) & 1));
-      if (tstamp) tstamp[3] = gtimer();
+      if (tstamp && lane == 0) tstamp[3] = gtimer();
     }
   } else if (warp >= 4) {
     // ===================== softmax + epilogue =====================
@@ -285,9 +312,10 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       uint32_t qw[QW];
       const int64_t grow = q_row0 + row;
       const uint4* src = reinterpret_cast<const uint4*>(P.q + (h * g.T + grow) * D + half * (D / 2));
+      const uint64_t once = ptx::policy_evict_first();   // each Q row is read by one tile only
 #pragma unroll
       for (int i = 0; i < QW / 4; ++i) {
-        const uint4 x = grow < g.T ? __ldg(src + i) : make_uint4(0, 0, 0, 0);
+        const uint4 x = grow < g.T ? ptx::ld_stream(src + i, once) : make_uint4(0, 0, 0, 0);
         qw[4 * i] = x.x; qw[4 * i + 1] = x.y; qw[4 * i + 2] = x.z; qw[4 * i + 3] = x.w;
       }
       if constexpr (QW == 32) {
@@ -308,7 +336,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         m = e & 0xFFFFFF;
         member = (e >> (24 + sub)) & 1;
       } else {
-        m = j;
+        m = m_first + j;
         member = true;
       }
       const int len = (m == g.M - 1 && g.n_text > 0) ? (int)g.last_len : (int)g.B;
@@ -351,7 +379,10 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         m_run = m_blk;
       }
       const float base_m = (m_run == -INFINITY) ? 0.f : m_run;
-      float sum4[4] = {0.f, 0.f, 0.f, 0.f};
+      // packed pairs: one FFMA2 (scale, subtract), two ex2, one FADD2 (row
+      // sum), one bf16x2 pack per two scores
+      const float2 sc2 = make_float2(sl2, sl2), nb2 = make_float2(-base_m, -base_m);
+      float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
       for (int c = 0; c < HC / 32; ++c) {
         uint32_t pk[16];
@@ -359,16 +390,16 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         for (int i = 0; i < 16; ++i) {
           // EMU of every 8 element pairs go to the FMA pipe, the rest to MUFU
           const bool emu = (i & 7) < EMU;
-          const float x0 = fmaf(__uint_as_float(sr[c][2 * i]), sl2, -base_m);
-          const float x1 = fmaf(__uint_as_float(sr[c][2 * i + 1]), sl2, -base_m);
-          const float p0 = emu ? ptx::ex2_poly(x0) : ptx::ex2(x0);
-          const float p1 = emu ? ptx::ex2_poly(x1) : ptx::ex2(x1);
-          sum4[i & 3] += p0 + p1;
-          pk[i] = ptx::pack_bf16(p0, p1);
+          const float2 x = ptx::ffma2(make_float2(__uint_as_float(sr[c][2 * i]), __uint_as_float(sr[c][2 * i + 1])),
+                                      sc2, nb2);
+          const float2 p = emu ? ptx::ex2_poly2(x) : make_float2(ptx::ex2(x.x), ptx::ex2(x.y));
+          sum2[i & 1] = ptx::fadd2(sum2[i & 1], p);
+          pk[i] = ptx::pack_bf16(p.x, p.y);
         }
         ptx::tmem_st16(s_addr + half * (HC / 2) + c * 16, pk);
       }
-      l_part = l_part * alpha + ((sum4[0] + sum4[1]) + (sum4[2] + sum4[3]));
+      const float2 st2 = ptx::fadd2(sum2[0], sum2[1]);
+      l_part = l_part * alpha + (st2.x + st2.y);
       // tcgen05.ld/st are warp-collective (.sync.aligned): the correction runs
       // for the whole warp whenever any of its rows needs it
       if (__any_sync(0xffffffffu, rescale_o)) {
@@ -404,15 +435,35 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     }
     const bool valid = row < rows_valid;
     const int64_t grow = q_row0 + row;
+    if (text) {
+      // split-K text chunk: unnormalised O (fp32), row max (log2 domain) and
+      // row sum of this chunk; text_combine_kernel produces the output row
+      float* po = P.text_part + (part * 128 + row) * D;
+#pragma unroll
+      for (int c = 0; c < HD / 32; ++c) {
+        uint32_t o[32];
+        const int col0 = half * HD + c * 32;
+        ptx::tmem_ld32(lane_base + C::O_COL + col0, o);
+        ptx::tmem_ld_wait();
+        if (valid) {
+#pragma unroll
+          for (int v4 = 0; v4 < 8; ++v4)
+            *reinterpret_cast<uint4*>(po + col0 + v4 * 4) =
+                make_uint4(o[v4 * 4], o[v4 * 4 + 1], o[v4 * 4 + 2], o[v4 * 4 + 3]);
+        }
+      }
+      if (valid && half == 0) P.text_ml[part * 128 + row] = make_float2(m_run, l_run);
+    } else {
     float rfac = 1.f;
     const double* comp = nullptr;
-    if (!text && P.rectify && valid) {
+    if (P.rectify && valid) {
       const int64_t n_blk = grow / g.B;
       rfac = P.ws.r_eff[h * g.N + n_blk];
       comp = P.ws.comp + (h * g.N + n_blk) * D;
     }
     const float inv_l = (count > 0 && l_run > 0.f) ? 1.f / l_run : 0.f;
     __nv_bfloat16* orow = P.out + (h * g.T + grow) * D;
+    const uint64_t once = ptx::policy_evict_first();
 #pragma unroll
     for (int c = 0; c < HD / 32; ++c) {
       uint32_t o[32];
@@ -434,13 +485,14 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
             }
             w[i] = ptx::pack_bf16(y0, y1);
           }
-          *reinterpret_cast<uint4*>(orow + col0 + v8 * 8) = make_uint4(w[0], w[1], w[2], w[3]);
+          ptx::st_stream(orow + col0 + v8 * 8, make_uint4(w[0], w[1], w[2], w[3]), once);
         }
       }
     }
     if (tstamp && sw == 0 && lane == 0) tstamp[5] = gtimer();
     if (valid && half == 0 && P.lse && !tstamp)
       P.lse[h * g.T + grow] = l_run > 0.f ? (log2f(l_run) + m_run) * 0.69314718055994531f : -INFINITY;
+    }
   }
 
   __syncwarp();
@@ -451,6 +503,49 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     ptx::tc_fence_after();
     ptx::tmem_dealloc<C::TMEM_COLS>(tmem);
   }
+}
+
+// Split-K text tiles: merge the chunks' (O_c, m_c, l_c) of every text query
+// row into the final row, O = sum_c 2^(m_c - m*) O_c / sum_c 2^(m_c - m*) l_c
+// (the online-softmax merge, kernel.py:120-145 semantics), plus the LSE.
+template <int D>
+__global__ void __launch_bounds__(256) text_combine_kernel(const float* __restrict__ part,
+                                                           const float2* __restrict__ ml,
+                                                           __nv_bfloat16* __restrict__ out, float* lse,
+                                                           Geometry g, int64_t tiles, int64_t chunks) {
+  const int64_t ht = blockIdx.x;                 // (head, text tile)
+  const int64_t h = ht / tiles, t = ht % tiles;
+  const int row = threadIdx.x / 2, half = threadIdx.x % 2;
+  const int64_t trow = t * 128 + row;
+  if (trow >= g.Tt) return;
+  const int64_t base = ht * chunks;
+  float mx = -INFINITY;
+  for (int64_t c = 0; c < chunks; ++c) mx = fmaxf(mx, ml[(base + c) * 128 + row].x);
+  float acc[D / 2];
+#pragma unroll
+  for (int i = 0; i < D / 2; ++i) acc[i] = 0.f;
+  float l = 0.f;
+  for (int64_t c = 0; c < chunks; ++c) {
+    const float2 e = ml[(base + c) * 128 + row];
+    const float w = e.x == -INFINITY ? 0.f : exp2f(e.x - mx);
+    l += w * e.y;
+    const float4* po = reinterpret_cast<const float4*>(part + ((base + c) * 128 + row) * D + half * (D / 2));
+#pragma unroll
+    for (int i = 0; i < D / 8; ++i) {
+      const float4 x = po[i];
+      acc[4 * i] += w * x.x; acc[4 * i + 1] += w * x.y; acc[4 * i + 2] += w * x.z; acc[4 * i + 3] += w * x.w;
+    }
+  }
+  const float inv = l > 0.f ? 1.f / l : 0.f;
+  __nv_bfloat16* orow = out + (h * g.T + g.Tv + trow) * D + half * (D / 2);
+#pragma unroll
+  for (int i = 0; i < D / 16; ++i) {
+    uint32_t w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) w[k] = ptx::pack_bf16(acc[8 * i + 2 * k] * inv, acc[8 * i + 2 * k + 1] * inv);
+    *reinterpret_cast<uint4*>(orow + 8 * i) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  if (lse && half == 0) lse[h * g.T + g.Tv + trow] = l > 0.f ? (log2f(l) + mx) * 0.69314718055994531f : -INFINITY;
 }
 
 // V [H][T][d] -> V^T [H][d][T] through a padded 64x64 shared-memory tile
@@ -538,15 +633,22 @@ cudaError_t launch_cfg(const Geometry& g, const void* q, const void* k, const vo
   P.trace_cta = tc_cta ? atoi(tc_cta) : 5000;
   P.lse = lse;
   P.rectify = rectify ? 1 : 0;
-  P.text_tiles_per_head = (g.Tt + 127) / 128;
-  P.n_text_tiles = text ? g.H * P.text_tiles_per_head : 0;
+  P.text_tiles_per_head = text ? (g.Tt + 127) / 128 : 0;
+  P.text_chunks = text_chunks(g);
+  P.chunk_blocks = (g.M + P.text_chunks - 1) / P.text_chunks;
   P.video_tiles_per_head = (g.N * g.B + 127) / 128;
+  P.tiles_per_head = P.text_tiles_per_head * P.text_chunks + P.video_tiles_per_head;
+  P.text_part = ws.text_part;
+  P.text_ml = reinterpret_cast<float2*>(ws.text_ml);
   P.scale_log2 = (float)(1.4426950408889634 / sqrt((double)g.d));
   auto kern = attn_tc_kernel<D, BKV, QTM, VT, EMU>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   if (e != cudaSuccess) return e;
-  const int64_t tiles = P.n_text_tiles + g.H * P.video_tiles_per_head;
-  kern<<<(unsigned)tiles, kThreads, C::SMEM, st>>>(tq, tk, tv, P);
+  kern<<<(unsigned)(g.H * P.tiles_per_head), kThreads, C::SMEM, st>>>(tq, tk, tv, P);
+  e = cudaGetLastError();
+  if (e != cudaSuccess || P.text_tiles_per_head == 0) return e;
+  text_combine_kernel<D><<<(unsigned)(g.H * P.text_tiles_per_head), 256, 0, st>>>(
+      P.text_part, P.text_ml, P.out, lse, g, P.text_tiles_per_head, P.text_chunks);
   return cudaGetLastError();
 }
 
@@ -560,12 +662,20 @@ bool tc_supported(const Geometry& g) {
 cudaError_t launch_attn_tc(const Geometry& g, const void* q, const void* k, const void* v, void* out, float* lse,
                            const Workspace& ws, bool rectify, bool text, cudaStream_t st, int* launches) {
   static const bool vt_on = [] { const char* e = getenv("RSA_TC_VT"); return e && atoi(e) != 0; }();
-  *launches += vt_on ? 2 : 1;   // (V transpose) + attention
+  *launches += (vt_on ? 2 : 1) + (text && g.Tt > 0 ? 1 : 0);   // (V transpose) + attention (+ text combine)
   // Variant knobs (profiling): RSA_TC_QTMEM=1 keeps Q in TMEM (2 S buffers);
   // RSA_TC_VT=0 streams V as an MN-major operand instead of V^T.
   static const int qtm = [] { const char* e = getenv("RSA_TC_QTMEM"); return e ? atoi(e) : 1; }();
   static const int vt = [] { const char* e = getenv("RSA_TC_VT"); return e ? atoi(e) : 0; }();
+  // RSA_TC_EMU=n: n of every 8 exp2 pairs on the FMA pipe (polynomial) instead of MUFU
+  static const int emu = [] { const char* e = getenv("RSA_TC_EMU"); return e ? atoi(e) : 0; }();
   const int sel = (qtm ? 2 : 0) + (vt ? 1 : 0);
+  if (qtm && !vt && g.d == 128 && g.B == 128 && emu == 1)
+    return launch_cfg<128, 128, true, false, 1>(g, q, k, v, out, lse, ws, rectify, text, st);
+  if (qtm && !vt && g.d == 128 && g.B == 128 && emu == 2)
+    return launch_cfg<128, 128, true, false, 2>(g, q, k, v, out, lse, ws, rectify, text, st);
+  if (qtm && !vt && g.d == 128 && g.B == 128 && emu == 3)
+    return launch_cfg<128, 128, true, false, 3>(g, q, k, v, out, lse, ws, rectify, text, st);
 #define RSA_TC_CASE(DD, BB)                                                                          \
   if (g.d == DD && g.B == BB) {                                                                      \
     switch (sel) {                                                                                   \

@@ -104,6 +104,9 @@ void layout_of(const rsa::Geometry& g, rsa_workspace_layout* L) {
   L->tile_count = take(H * TT * 4);
   L->tile_list = take(H * TT * M * 4);
   L->v_t = take(g.dtype == RSA_BF16 ? H * (size_t)((g.T + 7) / 8 * 8) * d * 2 : 0);   // pitch % 8 == 0
+  const size_t text_parts = g.dtype == RSA_BF16 ? H * (size_t)((g.Tt + 127) / 128) * rsa::text_chunks(g) * 128 : 0;
+  L->text_part = take(text_parts * d * 4);
+  L->text_ml = take(text_parts * 8);
   L->total = off;
 }
 
@@ -129,6 +132,8 @@ rsa::Workspace bind(const rsa::Geometry& g, void* base) {
   w.tile_count = reinterpret_cast<int32_t*>(b + L.tile_count);
   w.tile_list = reinterpret_cast<int32_t*>(b + L.tile_list);
   w.v_t = reinterpret_cast<__nv_bfloat16*>(b + L.v_t);
+  w.text_part = reinterpret_cast<float*>(b + L.text_part);
+  w.text_ml = reinterpret_cast<float*>(b + L.text_ml);
   return w;
 }
 

@@ -28,6 +28,8 @@ struct Workspace {
   int32_t* tile_count;
   int32_t* tile_list;
   __nv_bfloat16* v_t;   // [H][d][T] transposed V (tcgen05 path)
+  float* text_part;     // [H][text tiles][chunks][128][d] split-K text partial O (tcgen05 path)
+  float* text_ml;       // [H][text tiles][chunks][128][2] partial row max (log2) and sum
   int32_t* status;
 };
 
@@ -48,6 +50,10 @@ enum MaskBit : uint8_t {
 enum StatusFlag { ST_DEGENERATE = 0, ST_EMPTY_ROW = 1, ST_DEFICIT = 2 };
 
 constexpr int kTcTileRows = 128;   // query rows per tcgen05 tile (UMMA M)
+
+// kv-block chunks per 128-row text query tile of the tcgen05 kernel (split-K:
+// a text tile walks every kv block, ~10x a video tile's retained list)
+inline int64_t text_chunks(const Geometry& g) { return g.M > 128 ? (g.M + 127) / 128 : 1; }
 
 // ---- dtype helpers ---------------------------------------------------------
 template <typename T> struct Acc { using type = float; };

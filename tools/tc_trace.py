@@ -27,11 +27,15 @@ for _ in range(2):
     nat.check(lib.rsa_forward(C.byref(shape), C.byref(conf), _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse),
                               _ptr(ws), _stream()))
 torch.cuda.synchronize()
-tiles = heads * 2 + heads * 928
+tiles = heads * (2 * 8 + 928)   # text chunks (2 tiles x 8 chunks) + video tiles per head
 tr = lse.view(torch.int64)[tiles * 8: tiles * 8 + 64 * 8].view(64, 8).cpu().numpy().astype(np.int64)
 t0 = tr[0, 6]
-names = ["mma:K_j ready", "mma:P_j ready", "mma:V_j ready", "sm:S_j ready", "sm:max exch", "sm:P_j done",
-         "ld:K_j slot", "ld:V_j slot"]
+if os.environ.get("RSA_TC_KERNEL", "2") == "2":
+    names = ["mma:K_i ready", "mma:P_i ready", "mma:PV issued", "sm:S_i ready", "sm:S_i loaded", "sm:P_i done",
+             "ld:K_i slot", "ld:V_i slot"]
+else:
+    names = ["mma:K_j ready", "mma:P_j ready", "mma:V_j ready", "sm:S_j ready", "sm:max exch", "sm:P_j done",
+             "ld:K_j slot", "ld:V_j slot"]
 print("step " + " ".join(f"{n:>14s}" for n in names))
 for j in range(0, 40):
     print(f"{j:4d} " + " ".join(f"{(x - t0) if x else -1:14d}" for x in tr[j]))
