@@ -142,6 +142,18 @@ rsa_status rsa_forward(const rsa_shape* shape, const rsa_config* cfg, const void
                        const void* k, const void* v, void* out, float* lse,
                        void* workspace, void* stream);
 
+/* rsa_forward from HOST memory (end-to-end call): host_q/k/v/out are host
+ * pointers (page-locked for the copies to overlap), dq/dk/dv/dout device
+ * buffers of the same [heads][T][d] size.  Heads are processed in chunks of
+ * `heads_per_chunk`: chunk c+1's host->device copy and chunk c-1's
+ * device->host copy run on two internal streams while chunk c computes on
+ * `stream`.  Work is enqueued on `stream`; the output is in host memory once
+ * `stream` reaches the end of the call. */
+rsa_status rsa_forward_host(const rsa_shape* shape, const rsa_config* cfg, const void* host_q,
+                            const void* host_k, const void* host_v, void* host_out, void* dq,
+                            void* dk, void* dv, void* dout, float* lse, void* workspace,
+                            int64_t heads_per_chunk, void* stream);
+
 /* Kernel-only seam (kernel.py:65-117): video queries over an explicit block
  * mask (u8 [heads][N][M], nonzero = retained); no rectification.  Text rows
  * of `out` are left untouched. */

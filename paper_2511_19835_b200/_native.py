@@ -21,7 +21,7 @@ VARIANT_CODES = {"full": 0, "sparse-unrectified": 1, "sparse-rectified": 2,
 KERNEL_CODES = {"auto": 0, "tcgen05": 1, "simt": 2}
 
 EXPORTS = ("rsa_plan", "rsa_workspace_layout_query", "rsa_workspace_size", "rsa_pool",
-           "rsa_select", "rsa_attention", "rsa_forward", "rsa_block_sparse_attention",
+           "rsa_select", "rsa_attention", "rsa_forward", "rsa_forward_host", "rsa_block_sparse_attention",
            "rsa_text_full_attention", "rsa_check_device_status", "rsa_last_launch_count",
            "rsa_last_error", "rsa_version")
 
@@ -76,6 +76,8 @@ def lib() -> C.CDLL:
         "rsa_select": ([C.POINTER(Shape), C.POINTER(Config), P, P], C.c_int),
         "rsa_attention": ([C.POINTER(Shape), C.POINTER(Config), P, P, P, P, P, P, P], C.c_int),
         "rsa_forward": ([C.POINTER(Shape), C.POINTER(Config), P, P, P, P, P, P, P], C.c_int),
+        "rsa_forward_host": ([C.POINTER(Shape), C.POINTER(Config), P, P, P, P, P, P, P, P, P, P,
+                              C.c_int64, P], C.c_int),
         "rsa_block_sparse_attention": ([C.POINTER(Shape), P, P, P, P, P, P, P, P], C.c_int),
         "rsa_text_full_attention": ([C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
                                      C.c_int32, P, P, P, P, P, P, P], C.c_int),

@@ -12,7 +12,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <string>
+#include <vector>
 
 namespace {
 
@@ -258,6 +260,74 @@ rsa_status rsa_forward(const rsa_shape* shape, const rsa_config* cfg, const void
   s = rsa_select(shape, cfg, workspace, stream);
   if (s != RSA_OK) return s;
   return rsa_attention(shape, cfg, q, k, v, out, lse, workspace, stream);
+}
+
+// End-to-end call from host memory: heads are processed in chunks so chunk
+// c+1's host->device copy (copy-in stream) overlaps chunk c's K1->K2->K3
+// (caller's stream) and chunk c-1's device->host copy (copy-out stream).
+rsa_status rsa_forward_host(const rsa_shape* shape, const rsa_config* cfg, const void* host_q,
+                            const void* host_k, const void* host_v, void* host_out, void* dq, void* dk,
+                            void* dv, void* dout, float* lse, void* workspace, int64_t heads_per_chunk,
+                            void* stream) {
+  rsa::Geometry g;
+  rsa_status s = make_geometry(shape, &g);
+  if (s != RSA_OK) return s;
+  s = check_config(cfg);
+  if (s != RSA_OK) return s;
+  if (!host_q || !host_k || !host_v || !host_out || !dq || !dk || !dv || !dout || !workspace)
+    return fail(RSA_ERR_SHAPE, "null pointer");
+  if (heads_per_chunk < 1 || heads_per_chunk > g.H) heads_per_chunk = g.H;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  static thread_local cudaStream_t s_in = nullptr, s_out = nullptr;
+  static thread_local int dev_of_streams = -1;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  if (dev_of_streams != dev) {
+    if ((e = cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking)) != cudaSuccess)
+      return cuda_fail(e, "stream create");
+    dev_of_streams = dev;
+  }
+  const size_t esz = g.dtype == RSA_BF16 ? 2 : g.dtype == RSA_F32 ? 4 : 8;
+  const size_t head_bytes = (size_t)g.T * g.d * esz;
+  const int64_t n_chunks = (g.H + heads_per_chunk - 1) / heads_per_chunk;
+  std::vector<cudaEvent_t> ev(3 * n_chunks + 1);
+  for (auto& x : ev)
+    if ((e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(e, "event");
+  // the copy-in stream starts after whatever the caller queued on `stream`
+  cudaEventRecord(ev[3 * n_chunks], st);
+  cudaStreamWaitEvent(s_in, ev[3 * n_chunks], 0);
+  int launches = 0;
+  for (int64_t c = 0; c < n_chunks && s == RSA_OK; ++c) {
+    const int64_t h0 = c * heads_per_chunk, hc = std::min(heads_per_chunk, g.H - h0);
+    const size_t off = (size_t)h0 * head_bytes, bytes = (size_t)hc * head_bytes;
+    auto H = [&](const void* p) { return static_cast<const char*>(p) + off; };
+    auto D = [&](void* p) { return static_cast<char*>(p) + off; };
+    cudaMemcpyAsync(D(dq), H(host_q), bytes, cudaMemcpyHostToDevice, s_in);
+    cudaMemcpyAsync(D(dk), H(host_k), bytes, cudaMemcpyHostToDevice, s_in);
+    if ((e = cudaMemcpyAsync(D(dv), H(host_v), bytes, cudaMemcpyHostToDevice, s_in)) != cudaSuccess)
+      return cuda_fail(e, "H2D");
+    cudaEventRecord(ev[3 * c], s_in);
+    cudaStreamWaitEvent(st, ev[3 * c], 0);
+    rsa_shape sub = *shape;
+    sub.heads = hc;
+    s = rsa_forward(&sub, cfg, D(dq), D(dk), D(dv), D(dout), lse ? lse + h0 * g.T : nullptr, workspace, stream);
+    launches += g_launches;
+    cudaEventRecord(ev[3 * c + 1], st);
+    cudaStreamWaitEvent(s_out, ev[3 * c + 1], 0);
+    if ((e = cudaMemcpyAsync(static_cast<char*>(host_out) + off, D(dout), bytes, cudaMemcpyDeviceToHost,
+                             s_out)) != cudaSuccess)
+      return cuda_fail(e, "D2H");
+    cudaEventRecord(ev[3 * c + 2], s_out);
+  }
+  // the caller's stream resumes once every output chunk is in host memory
+  for (int64_t c = 0; c < n_chunks; ++c) cudaStreamWaitEvent(st, ev[3 * c + 2], 0);
+  for (auto& x : ev) cudaEventDestroy(x);
+  g_launches = launches;
+  if (s != RSA_OK) return s;
+  e = cudaGetLastError();
+  return e == cudaSuccess ? RSA_OK : cuda_fail(e, "forward_host");
 }
 
 rsa_status rsa_block_sparse_attention(const rsa_shape* shape, const void* q, const void* k,

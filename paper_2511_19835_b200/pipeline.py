@@ -237,11 +237,14 @@ def rectified_sparse_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor
                                variant: str = "sparse-rectified", sparsity: float | None = None,
                                kernel: str = "auto", lse: torch.Tensor | None = None,
                                workspace: torch.Tensor | None = None,
-                               check_status: bool = False) -> torch.Tensor:
+                               check_status: bool = False, heads_per_chunk: int = 1) -> torch.Tensor:
     """Rectified block-sparse attention for every (batch, head) of q/k/v
     ([..., T, d], the last ``num_text_tokens`` rows text).  ``sparsity=s`` is
     shorthand for top_k_fraction = 1 - s with p = 0, r = 0, no forced text.
-    Stream-ordered; no host synchronisation unless ``check_status``."""
+    CUDA tensors: stream-ordered, no host synchronisation unless
+    ``check_status``.  Host tensors (the end-to-end call): the copies in and
+    out are pipelined with the compute over chunks of ``heads_per_chunk``
+    heads (rsa_forward_host) and the host output is returned."""
     if sparsity is not None:
         top_k_fraction, weight_threshold, adjacency_radius, force_text_blocks = 1.0 - sparsity, 0.0, 0, False
     if top_k_fraction is None:
@@ -249,14 +252,16 @@ def rectified_sparse_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor
     if q.dim() < 3 or q.shape != k.shape or k.shape != v.shape:
         raise ShapeError(f"q/k/v must share a [..., T, d] shape, got {tuple(q.shape)}, "
                          f"{tuple(k.shape)}, {tuple(v.shape)}")
-    if not q.is_cuda:
-        raise NativeError("rectified_sparse_attention needs CUDA tensors (no CPU fallback)")
     T, d = q.shape[-2], q.shape[-1]
     heads = int(np.prod(q.shape[:-2]))
     t_t = int(num_text_tokens)
     shape = nat.make_shape(heads, T - t_t, t_t, d, block, str(q.dtype).replace("torch.", ""), kernel)
     cfg = nat.make_config(top_k_fraction, weight_threshold, adjacency_radius, force_text_blocks, variant)
     nat.plan(shape, cfg)
+    if not q.is_cuda:
+        if k.is_cuda or v.is_cuda:
+            raise ShapeError("q, k and v must all be host tensors or all CUDA tensors")
+        return _forward_from_host(q, k, v, shape, cfg, lse, workspace, heads_per_chunk)
     q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
     if workspace is None:
         workspace = workspace_for(shape, q.device)
@@ -265,4 +270,33 @@ def rectified_sparse_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor
                                     _ptr(out), _ptr(lse), _ptr(workspace), _stream()))
     if check_status:
         nat.check(nat.lib().rsa_check_device_status(_ptr(workspace), _stream()))
+    return out
+
+
+_STAGING: dict = {}
+
+
+def _forward_from_host(q, k, v, shape, cfg, lse, workspace, heads_per_chunk):
+    """Host tensors in, host tensor out: rsa_forward_host pipelines the
+    host->device copies, the three kernels and the device->host copy over
+    chunks of heads.  Inputs should be page-locked (``pin_memory()``) for the
+    copies to overlap the compute; the staging buffers are cached per shape."""
+    dev = _device()
+    if not torch.cuda.is_available():
+        raise NativeError("no CUDA device (there is no CPU fallback)")
+    q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+    key = (tuple(q.shape), q.dtype, dev.index)
+    bufs = _STAGING.get(key)
+    if bufs is None:
+        _STAGING.clear()
+        bufs = [torch.empty(q.shape, dtype=q.dtype, device=dev) for _ in range(4)]
+        _STAGING[key] = bufs
+    dq, dk, dv, dout = bufs
+    if workspace is None:
+        workspace = workspace_for(shape, dev)
+    out = torch.empty(q.shape, dtype=q.dtype, pin_memory=q.is_pinned())
+    nat.check(nat.lib().rsa_forward_host(C.byref(shape), C.byref(cfg), _ptr(q), _ptr(k), _ptr(v), _ptr(out),
+                                         _ptr(dq), _ptr(dk), _ptr(dv), _ptr(dout), _ptr(lse),
+                                         _ptr(workspace), int(heads_per_chunk), _stream()))
+    torch.cuda.current_stream().synchronize()
     return out
