@@ -16,6 +16,8 @@
 // independent of launch geometry.
 #include "rsa_internal.cuh"
 
+#include <algorithm>
+
 namespace rsa {
 namespace {
 
@@ -219,6 +221,234 @@ pool_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restric
   }
 }
 
+// ---------------------------------------------------------------------------
+// bf16 fast path: persistent CTAs stream whole blocks (B rows x d bf16, one
+// contiguous B*d*2-byte range of [H][T][d]) into a shared-memory ring with 1-D
+// bulk async copies (cp.async.bulk, TMA engine), several blocks in flight per
+// CTA, and reduce them from shared memory.  The exactness argument is the one
+// of pool_kernel (pass 1): bf16 values have p = 8 significant bits, so fp64
+// partial sums are exact while e_max - e_min + 8 + ceil(log2 len) < 53; a
+// block that fails the test (never for sane data) is re-summed from the same
+// shared-memory copy with TwoSum pairs.  Bit-identical to math.fsum either way.
+// ---------------------------------------------------------------------------
+constexpr int kBulkThreads = 256;
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          (uint32_t)__cvta_generic_to_shared(dst)),
+      "l"(src), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
+               "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void bar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(parity)
+        : "memory");
+  }
+}
+
+struct PoolItem {
+  int64_t h, blk;
+  int seg;
+};
+
+// items: per head [N Q video blocks][M K blocks][M V blocks]
+__device__ __forceinline__ PoolItem pool_item(const Geometry& g, int64_t i) {
+  const int64_t per_head = g.N + 2 * g.M;
+  PoolItem it;
+  it.h = i / per_head;
+  int64_t r = i % per_head;
+  if (r < g.N) { it.seg = 0; it.blk = r; }
+  else if (r < g.N + g.M) { it.seg = 1; it.blk = r - g.N; }
+  else { it.seg = 2; it.blk = r - g.N - g.M; }
+  return it;
+}
+
+template <int D, int STAGES>
+__global__ void __launch_bounds__(kBulkThreads, 2)
+pool_bulk_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k,
+                 const __nv_bfloat16* __restrict__ v, Workspace ws, Geometry g, int64_t n_items) {
+  constexpr int WPR = D / 2;                   // 32-bit words (bf16 pairs) per row
+  constexpr int RP = kBulkThreads / WPR;       // row phases
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int stage_bytes = (int)(g.B * D * 2);
+  uint8_t* ring = smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * stage_bytes);
+  double* s_part = reinterpret_cast<double*>(full + STAGES);     // [RP][D] hi (+ [RP][D] lo)
+  float* s_rng = reinterpret_cast<float*>(s_part + 2 * RP * D);  // [8 warps][2]
+  __shared__ int s_exact;
+
+  const int t = threadIdx.x;
+  const int word = t % WPR, rp = t / WPR;
+  auto src_of = [&](const PoolItem& it, uint32_t& bytes) -> const void* {
+    const int64_t len = (it.blk < g.N) ? g.B : (it.blk == g.M - 1 ? g.last_len : g.B);
+    bytes = (uint32_t)(len * D * 2);
+    const __nv_bfloat16* base = it.seg == 0 ? q : it.seg == 1 ? k : v;
+    return base + (it.h * g.T + it.blk * g.B) * D;
+  };
+  if (t == 0) {
+    for (int s = 0; s < STAGES; ++s) bar_init(full + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (t == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      const int64_t i = blockIdx.x + (int64_t)s * gridDim.x;
+      if (i >= n_items) break;
+      uint32_t bytes;
+      const void* src = src_of(pool_item(g, i), bytes);
+      bar_expect_tx(full + s, bytes);
+      bulk_g2s(ring + s * stage_bytes, src, bytes, full + s);
+    }
+  }
+  int64_t kk = 0;
+  for (int64_t i = blockIdx.x; i < n_items; i += gridDim.x, ++kk) {
+    const int s = (int)(kk % STAGES);
+    const PoolItem it = pool_item(g, i);
+    const int64_t len = (it.blk < g.N) ? g.B : (it.blk == g.M - 1 ? g.last_len : g.B);
+    bar_wait(full + s, (uint32_t)((kk / STAGES) & 1));
+    const uint32_t* blk = reinterpret_cast<const uint32_t*>(ring + s * stage_bytes);
+    // pass 1: plain fp64 sums of this thread's column pair over its row phase,
+    // plus the magnitude range (bf16 bits & 0x7FFF is monotonic in |x|)
+    double a0 = 0.0, a1 = 0.0;
+    uint32_t bmax = 0, bmin = 0xFFFFu;
+    const bool text_k = (it.seg == 1) && (it.blk >= g.N);
+    double* raw_out = text_k ? ws.k_cat + (it.h * g.n_cols + g.N + (it.blk * g.B - g.Tv)) * D : nullptr;
+#pragma unroll 8
+    for (int64_t r = rp; r < len; r += RP) {
+      const uint32_t w = blk[r * WPR + word];
+      const float x0 = __uint_as_float(w << 16), x1 = __uint_as_float(w & 0xFFFF0000u);
+      a0 += (double)x0;
+      a1 += (double)x1;
+      const uint32_t m0 = w & 0x7FFFu, m1 = (w >> 16) & 0x7FFFu;
+      bmax = max(bmax, max(m0, m1));
+      bmin = min(bmin, min(m0 ? m0 : 0xFFFFu, m1 ? m1 : 0xFFFFu));
+      if (raw_out) {
+        raw_out[r * D + 2 * word] = (double)x0;
+        raw_out[r * D + 2 * word + 1] = (double)x1;
+      }
+    }
+    s_part[rp * D + 2 * word] = a0;
+    s_part[rp * D + 2 * word + 1] = a1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      bmax = max(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
+      bmin = min(bmin, __shfl_xor_sync(0xffffffffu, bmin, o));
+    }
+    if (t % 32 == 0) {
+      reinterpret_cast<uint32_t*>(s_rng)[2 * (t / 32)] = bmax;
+      reinterpret_cast<uint32_t*>(s_rng)[2 * (t / 32) + 1] = bmin;
+    }
+    __syncthreads();
+    if (t == 0) {
+      uint32_t mx = 0, mn = 0xFFFFu;
+      for (int w = 0; w < kBulkThreads / 32; ++w) {
+        mx = max(mx, reinterpret_cast<uint32_t*>(s_rng)[2 * w]);
+        mn = min(mn, reinterpret_cast<uint32_t*>(s_rng)[2 * w + 1]);
+      }
+      int lg = 0;
+      while ((int64_t(1) << lg) < len) ++lg;
+      // exponent fields (bits >> 7); subnormals (field 0) count as exponent 1
+      const int emax = max(1, (int)(mx >> 7)), emin = max(1, (int)(mn >> 7));
+      s_exact = (mn == 0xFFFFu) || (emax - emin + 8 + lg < 53);
+    }
+    __syncthreads();
+    const bool exact = s_exact != 0;
+    if (!exact) {
+      // TwoSum (hi, lo) pairs over the same shared-memory copy
+      double h0 = 0.0, l0 = 0.0, h1 = 0.0, l1 = 0.0;
+      for (int64_t r = rp; r < len; r += RP) {
+        const uint32_t w = blk[r * WPR + word];
+        double sm, e;
+        two_sum(h0, (double)__uint_as_float(w << 16), sm, e); h0 = sm; l0 += e;
+        two_sum(h1, (double)__uint_as_float(w & 0xFFFF0000u), sm, e); h1 = sm; l1 += e;
+      }
+      s_part[rp * D + 2 * word] = h0;
+      s_part[rp * D + 2 * word + 1] = h1;
+      s_part[RP * D + rp * D + 2 * word] = l0;
+      s_part[RP * D + rp * D + 2 * word + 1] = l1;
+      __syncthreads();
+    }
+    // stage s is free: refill it with this CTA's item STAGES ahead
+    if (t == 0) {
+      const int64_t nx = i + (int64_t)STAGES * gridDim.x;
+      if (nx < n_items) {
+        uint32_t bytes;
+        const void* src = src_of(pool_item(g, nx), bytes);
+        bar_expect_tx(full + s, bytes);
+        bulk_g2s(ring + s * stage_bytes, src, bytes, full + s);
+      }
+    }
+    for (int col = t; col < D; col += kBulkThreads) {
+      double sum;
+      if (exact) {
+        sum = 0.0;
+        for (int p = 0; p < RP; ++p) sum += s_part[p * D + col];
+      } else {
+        double S = 0.0, E = 0.0;
+        for (int p = 0; p < RP; ++p) {
+          double sm, e;
+          two_sum(S, s_part[p * D + col], sm, e);
+          S = sm;
+          E += e + s_part[RP * D + p * D + col];
+        }
+        sum = S + E;
+      }
+      const double flen = (double)len;
+      const double mean = sum / flen;            // core.py:172 fsum(...) / length
+      const double deficit = sum - flen * mean;  // masks.py:166 / masks.py:171
+      if (it.seg == 0) {
+        ws.q_pool[(it.h * g.N + it.blk) * D + col] = mean;
+        ws.q_def[(it.h * g.N + it.blk) * D + col] = deficit;
+      } else if (it.seg == 1) {
+        const int64_t kc_row = it.blk < g.N ? it.blk : g.N + g.Tt + (it.blk - g.N);
+        ws.k_cat[(it.h * g.n_cols + kc_row) * D + col] = mean;
+        ws.k_def[(it.h * g.M + it.blk) * D + col] = deficit;
+      } else {
+        ws.v_pool[(it.h * g.M + it.blk) * D + col] = mean;
+      }
+      if (it.seg < 2 && deficit != 0.0) atomicOr(ws.status + ST_DEFICIT, 1);
+    }
+    __syncthreads();
+  }
+}
+
+template <int D>
+cudaError_t launch_bulk(const Geometry& g, const void* q, const void* k, const void* v, const Workspace& ws,
+                        cudaStream_t st) {
+  constexpr int STAGES = 3;
+  constexpr int RP = kBulkThreads / (D / 2);
+  const size_t smem = (size_t)STAGES * g.B * D * 2 + STAGES * 8 + 2 * RP * D * 8 + 64;
+  auto kern = pool_bulk_kernel<D, STAGES>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t n_items = g.H * (g.N + 2 * g.M);
+  const int64_t grid = std::min<int64_t>(n_items, (int64_t)sms * 2);
+  kern<<<(unsigned)grid, kBulkThreads, smem, st>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
+                                                   (const __nv_bfloat16*)v, ws, g, n_items);
+  return cudaGetLastError();
+}
+
 template <typename T>
 cudaError_t launch_typed(const Geometry& g, const void* q, const void* k, const void* v,
                          const Workspace& ws, cudaStream_t st) {
@@ -240,7 +470,15 @@ cudaError_t launch_pool(const Geometry& g, const void* q, const void* k, const v
                         const Workspace& ws, cudaStream_t st, int* launches) {
   ++*launches;
   switch (g.dtype) {
-    case RSA_BF16: return launch_typed<__nv_bfloat16>(g, q, k, v, ws, st);
+    case RSA_BF16: {
+      // bulk-copy streaming path when a block is one 16-byte-aligned range
+      // that fits three ring stages per CTA, two CTAs per SM
+      const bool aligned = ((uintptr_t)q % 16 == 0) && ((uintptr_t)k % 16 == 0) && ((uintptr_t)v % 16 == 0);
+      const bool fits = g.B * g.d * 2 * 3 <= 96 * 1024;
+      if (aligned && fits && g.d == 128) return launch_bulk<128>(g, q, k, v, ws, st);
+      if (aligned && fits && g.d == 64) return launch_bulk<64>(g, q, k, v, ws, st);
+      return launch_typed<__nv_bfloat16>(g, q, k, v, ws, st);
+    }
     case RSA_F32: return launch_typed<float>(g, q, k, v, ws, st);
     default: return launch_typed<double>(g, q, k, v, ws, st);
   }
