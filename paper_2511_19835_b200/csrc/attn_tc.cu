@@ -26,6 +26,7 @@
 #include "tc_ptx.cuh"
 
 #include <cuda.h>
+#include <algorithm>
 #include <cstdlib>
 #include <cudaTypedefs.h>
 
@@ -505,6 +506,412 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   }
 }
 
+// ============================================================================
+// Persistent variant (production path): one CTA per SM walks the tiles
+// blockIdx.x, blockIdx.x + gridDim.x, ... (head-major order, so the SMs work
+// on ~one head's K/V at a time).  TMEM allocation, barrier set-up and the
+// K/V ring persist across tiles; barrier phases and the S/P buffer index run
+// on per-CTA step counters.  At a tile boundary the softmax warps store the
+// next tile's Q rows into TMEM as soon as the last S of the current tile has
+// been read, so the MMA warp starts the next tile's S_0, S_1 while the same
+// warps run the current tile's epilogue; PV_0 of the next tile (which
+// overwrites O) waits for its P_0, i.e. after that epilogue.  This removes the
+// per-CTA launch gap (~8 us), set-up and Q-load latency of the one-tile
+// kernel (profiles/r01j: 16 us of ~117 us per tile).
+// ============================================================================
+struct TileDesc {
+  int64_t h, q_row0, rows_valid, count, m_first, part;
+  const int32_t* list;
+  bool text;
+};
+
+__device__ __forceinline__ TileDesc decode_tile(const TcParams& P, int64_t bid) {
+  const Geometry& g = P.g;
+  TileDesc t;
+  t.h = bid / P.tiles_per_head;
+  const int64_t r_in = bid % P.tiles_per_head;
+  const int64_t n_text_ct = P.text_tiles_per_head * P.text_chunks;
+  t.text = r_in < n_text_ct;
+  t.m_first = 0;
+  t.part = 0;
+  t.list = nullptr;
+  if (t.text) {
+    const int64_t tt = r_in / P.text_chunks, c = r_in % P.text_chunks;
+    t.q_row0 = g.Tv + tt * 128;
+    t.rows_valid = min((int64_t)128, g.Tt - tt * 128);
+    t.m_first = c * P.chunk_blocks;
+    t.count = min(g.M, t.m_first + P.chunk_blocks) - t.m_first;
+    t.part = (t.h * P.text_tiles_per_head + tt) * P.text_chunks + c;
+  } else {
+    const int64_t tt = r_in - n_text_ct;
+    t.q_row0 = tt * 128;
+    t.rows_valid = min((int64_t)128, g.Tv - t.q_row0);
+    t.count = P.ws.tile_count[t.h * P.video_tiles_per_head + tt];
+    t.list = P.ws.tile_list + (t.h * P.video_tiles_per_head + tt) * g.M;
+  }
+  return t;
+}
+
+template <int D, int BKV>
+__device__ __forceinline__ void producer_loop(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const TcParams& P,
+                                   int64_t n_tiles, uint8_t* kv_s, uint64_t* q_full, uint64_t* kv_full,
+                                   uint64_t* kv_empty, uint64_t* s_full, uint64_t* p_full, uint64_t* pv_done,
+                                   uint32_t tmem, int lane) {
+  using C = Cfg<D, BKV, true, false>;
+  const Geometry& g = P.g;
+  (void)g; (void)q_full; (void)s_full; (void)p_full; (void)pv_done; (void)tmem; (void)tm_v;
+  // ===================== TMA producer: every tile's K_0 K_1 V_0 K_2 V_1 ... =====================
+  if (lane == 0) {
+    ptx::prefetch_tmap(&tm_k);
+    ptx::prefetch_tmap(&tm_v);
+    const uint64_t keep = ptx::policy_evict_last();   // K/V blocks are re-read by many tiles of the head
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t bid = blockIdx.x; bid < n_tiles; bid += gridDim.x) {
+      const TileDesc t = decode_tile(P, bid);
+      auto load = [&](int64_t j, bool is_v) {
+        const int64_t m = t.list ? (t.list[j] & 0xFFFFFF) : t.m_first + j;
+        ptx::mbar_wait(kv_empty + s, ph ^ 1);
+        ptx::mbar_expect_tx(kv_full + s, C::STAGE);
+        uint8_t* dst = kv_s + s * C::STAGE;
+#pragma unroll
+        for (int p = 0; p < C::PANELS; ++p)
+          ptx::tma_load_3d_hint(dst + p * C::KV_PANEL, is_v ? &tm_v : &tm_k, kv_full + s, 64 * p,
+                                (int)(m * g.B), (int)t.h, keep);
+        if (++s == C::NST) { s = 0; ph ^= 1; }
+      };
+      for (int64_t j = 0; j <= t.count; ++j) {
+        if (j < t.count) load(j, false);
+        if (j >= 1) load(j - 1, true);
+      }
+    }
+  }
+}
+
+template <int D, int BKV>
+__device__ __forceinline__ void mma_loop(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const TcParams& P,
+                                   int64_t n_tiles, uint8_t* kv_s, uint64_t* q_full, uint64_t* kv_full,
+                                   uint64_t* kv_empty, uint64_t* s_full, uint64_t* p_full, uint64_t* pv_done,
+                                   uint32_t tmem, int lane) {
+  using C = Cfg<D, BKV, true, false>;
+  const Geometry& g = P.g;
+  (void)g; (void)q_full; (void)s_full; (void)p_full; (void)pv_done; (void)tmem; (void)tm_v;
+  // ===================== MMA issuer (whole warp; one elected lane issues) =====================
+  const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+  const uint32_t kv_addr = __shfl_sync(0xffffffffu, ptx::smem_u32(kv_s), 0);
+  int s_kv = 0;
+  uint32_t ph_kv = 0;
+  int64_t gs = 0;          // S/P steps issued by this CTA before the current tile
+  uint32_t tile_par = 0;
+  auto advance = [&]() {
+    if (++s_kv == C::NST) { s_kv = 0; ph_kv ^= 1u; }
+  };
+  for (int64_t bid = blockIdx.x; bid < n_tiles; bid += gridDim.x) {
+    const int64_t count = decode_tile(P, bid).count;
+    ptx::mbar_wait(q_full, tile_par);   // this tile's Q rows are in TMEM
+    tile_par ^= 1u;
+    ptx::tc_fence_after();
+    for (int64_t j = 0; j <= count; ++j) {
+      if (j < count) {
+        const int64_t gj = gs + j;
+        ptx::mbar_wait(kv_full + s_kv, ph_kv);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tm + (uint32_t)((gj % C::NS) * BKV);
+        const uint32_t kb = kv_addr + (uint32_t)(s_kv * C::STAGE);
+        if (ptx::elect_one()) {
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k) {
+            const uint64_t b = ptx::sw128_desc(kb + (k / 4) * C::KV_PANEL + (k % 4) * 32, 16, 1024);
+            ptx::mma_ts(d_tmem, tm + C::Q_COL + k * 8, b, C::IDESC_S, k > 0);
+          }
+          ptx::tc_commit(kv_empty + s_kv);
+          ptx::tc_commit(s_full + (gj % C::NS));
+        }
+        __syncwarp();
+        advance();
+      }
+      if (j >= 1) {
+        const int64_t gj = gs + j - 1;
+        ptx::mbar_wait(p_full + (gj % C::NS), (uint32_t)((gj / C::NS) & 1));
+        ptx::mbar_wait(kv_full + s_kv, ph_kv);
+        ptx::tc_fence_after();
+        const uint32_t a_tmem = tm + (uint32_t)((gj % C::NS) * BKV);
+        const uint32_t vb = kv_addr + (uint32_t)(s_kv * C::STAGE);
+        if (ptx::elect_one()) {
+#pragma unroll
+          for (int k = 0; k < BKV / 16; ++k) {
+            const uint64_t b = ptx::sw128_desc(vb + k * 2048, C::KV_PANEL, 1024);
+            ptx::mma_ts(tm + C::O_COL, a_tmem + k * 8, b, C::IDESC_O, (j > 1 || k > 0) ? 1u : 0u);
+          }
+          ptx::tc_commit(kv_empty + s_kv);
+          ptx::tc_commit(pv_done);
+        }
+        __syncwarp();
+        advance();
+      }
+    }
+    gs += count;
+  }
+}
+
+template <int D, int BKV>
+__global__ void __launch_bounds__(kThreads, 1)
+attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                          const TcParams P, int64_t n_tiles) {
+  using C = Cfg<D, BKV, true, false>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* kv_s = base;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(kv_s + C::NST * C::STAGE);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;
+  uint64_t* kv_empty = kv_full + C::NST;
+  uint64_t* s_full = kv_empty + C::NST;    // [NS]
+  uint64_t* p_full = s_full + C::NS;       // [NS]
+  uint64_t* pv_done = p_full + C::NS;      // [1]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 1);
+  float* red_max = reinterpret_cast<float*>(bars + 32);   // [2][2][128] row maxima + [2][128] row sums
+
+  const Geometry& g = P.g;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(q_full, 256);
+    for (int i = 0; i < C::NST; ++i) {
+      ptx::mbar_init(kv_full + i, 1);
+      ptx::mbar_init(kv_empty + i, 1);
+    }
+    for (int i = 0; i < C::NS; ++i) {
+      ptx::mbar_init(s_full + i, 1);
+      ptx::mbar_init(p_full + i, 256);
+    }
+    ptx::mbar_init(pv_done, 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    producer_loop<D, BKV>(tm_k, tm_v, P, n_tiles, kv_s, q_full, kv_full, kv_empty, s_full, p_full, pv_done, tmem, lane);
+  } else if (warp == 1) {
+    mma_loop<D, BKV>(tm_k, tm_v, P, n_tiles, kv_s, q_full, kv_full, kv_empty, s_full, p_full, pv_done, tmem, lane);
+  } else if (warp >= 4) {
+    // ===================== softmax + epilogue =====================
+    constexpr int HC = BKV / 2;     // score columns per thread
+    constexpr int HD = D / 2;       // output columns per thread
+    constexpr int QW = D / 4;       // 32-bit Q words per thread
+    const int sw = warp - 4;
+    const int quad = sw & 3, half = sw >> 2;
+    const int row = quad * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
+    const int sub = row / (int)g.B;          // which member query block of the tile
+    const float sl2 = P.scale_log2;
+    const uint64_t once = ptx::policy_evict_first();   // Q rows and outputs are touched once
+    // Q row -> TMEM lanes (A operand of S = Q K^T): this thread packs half of
+    // its row's d columns, bf16 pairs per 32-bit column
+    auto store_q = [&](const TileDesc& t) {
+      uint32_t qw[QW];
+      const int64_t grow = t.q_row0 + row;
+      const uint4* src = reinterpret_cast<const uint4*>(P.q + (t.h * g.T + grow) * D + half * (D / 2));
+#pragma unroll
+      for (int i = 0; i < QW / 4; ++i) {
+        const uint4 x = grow < g.T ? ptx::ld_stream(src + i, once) : make_uint4(0, 0, 0, 0);
+        qw[4 * i] = x.x; qw[4 * i + 1] = x.y; qw[4 * i + 2] = x.z; qw[4 * i + 3] = x.w;
+      }
+      if constexpr (QW == 32) {
+        ptx::tmem_st32(lane_base + C::Q_COL + half * QW, qw);
+      } else {
+        ptx::tmem_st16(lane_base + C::Q_COL + half * QW, qw);
+      }
+      ptx::tmem_st_wait();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(q_full);
+    };
+    int64_t gs = 0;
+    int64_t bid = blockIdx.x;
+    TileDesc t;
+    if (bid < n_tiles) {
+      t = decode_tile(P, bid);
+      store_q(t);
+    }
+    for (; bid < n_tiles; bid += gridDim.x) {
+      const int64_t count = t.count;
+      float m_run = -INFINITY, l_part = 0.f;
+      for (int64_t j = 0; j < count; ++j) {
+        const int64_t gj = gs + j;
+        int64_t m;
+        bool member;
+        if (t.list) {
+          const int32_t e = t.list[j];
+          m = e & 0xFFFFFF;
+          member = (e >> (24 + sub)) & 1;
+        } else {
+          m = t.m_first + j;
+          member = true;
+        }
+        const int len = (m == g.M - 1 && g.n_text > 0) ? (int)g.last_len : (int)g.B;
+        ptx::mbar_wait(s_full + (gj % C::NS), (uint32_t)((gj / C::NS) & 1));
+        ptx::tc_fence_after();
+        const uint32_t s_addr = lane_base + (uint32_t)((gj % C::NS) * BKV);
+        uint32_t sr[HC / 32][32];
+#pragma unroll
+        for (int c = 0; c < HC / 32; ++c) ptx::tmem_ld32(s_addr + half * HC + c * 32, sr[c]);
+        ptx::tmem_ld_wait();
+        if (!member || len < BKV) {
+#pragma unroll
+          for (int c = 0; c < HC / 32; ++c)
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (!member || half * HC + c * 32 + i >= len) sr[c][i] = __float_as_uint(-INFINITY);
+        }
+        float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int c = 0; c < HC / 32; ++c)
+#pragma unroll
+          for (int i = 0; i < 32; ++i) mx4[i & 3] = fmaxf(mx4[i & 3], __uint_as_float(sr[c][i]));
+        float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+        red_max[(gj & 1) * 256 + half * 128 + row] = mx;
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        mx = fmaxf(mx, red_max[(gj & 1) * 256 + (half ^ 1) * 128 + row]);
+        const float m_blk = mx * sl2;              // -inf if the row retains nothing here
+        const float m_old = m_run;
+        float alpha = 1.f;
+        bool rescale_o = false;
+        if (m_blk > m_run + kRescaleThreshold || (m_run == -INFINITY && m_blk > -INFINITY)) {
+          alpha = (m_old == -INFINITY) ? 0.f : ptx::ex2(m_old - m_blk);
+          rescale_o = (m_old != -INFINITY) && j > 0;
+          m_run = m_blk;
+        }
+        const float base_m = (m_run == -INFINITY) ? 0.f : m_run;
+        const float2 sc2 = make_float2(sl2, sl2), nb2 = make_float2(-base_m, -base_m);
+        float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+        for (int c = 0; c < HC / 32; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float2 x = ptx::ffma2(make_float2(__uint_as_float(sr[c][2 * i]), __uint_as_float(sr[c][2 * i + 1])),
+                                        sc2, nb2);
+            const float2 p = make_float2(ptx::ex2(x.x), ptx::ex2(x.y));
+            sum2[i & 1] = ptx::fadd2(sum2[i & 1], p);
+            pk[i] = ptx::pack_bf16(p.x, p.y);
+          }
+          ptx::tmem_st16(s_addr + half * (HC / 2) + c * 16, pk);
+        }
+        const float2 st2 = ptx::fadd2(sum2[0], sum2[1]);
+        l_part = l_part * alpha + (st2.x + st2.y);
+        if (__any_sync(0xffffffffu, rescale_o)) {
+          // O must hold exactly PV_0..PV_{j-1} of this tile before it is rescaled
+          ptx::mbar_wait(pv_done, (uint32_t)((gj - 1) & 1));
+          ptx::tc_fence_after();
+          const float a = rescale_o ? alpha : 1.f;
+#pragma unroll
+          for (int c = 0; c < HD / 32; ++c) {
+            uint32_t o[32];
+            const uint32_t oa = lane_base + C::O_COL + half * HD + c * 32;
+            ptx::tmem_ld32(oa, o);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * a);
+            ptx::tmem_st32(oa, o);
+          }
+        }
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(p_full + (gj % C::NS));
+      }
+      // every S of this tile has been read: Q's TMEM columns are free, so the
+      // next tile's Q goes in now and its S_0, S_1 overlap this epilogue
+      const TileDesc cur = t;
+      const int64_t nb = bid + gridDim.x;
+      if (nb < n_tiles) {
+        t = decode_tile(P, nb);
+        store_q(t);
+      }
+
+      // ---- epilogue: O / l, rectification (rectify.py:66-89), bf16 store, LSE ----
+      red_max[512 + half * 128 + row] = l_part;
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      const float l_run = l_part + red_max[512 + (half ^ 1) * 128 + row];
+      if (count > 0) {
+        ptx::mbar_wait(pv_done, (uint32_t)((gs + count - 1) & 1));
+        ptx::tc_fence_after();
+      }
+      const bool valid = row < cur.rows_valid;
+      const int64_t grow = cur.q_row0 + row;
+      if (cur.text) {
+        // split-K text chunk: unnormalised O (fp32), row max (log2) and row sum
+        float* po = P.text_part + (cur.part * 128 + row) * D;
+#pragma unroll
+        for (int c = 0; c < HD / 32; ++c) {
+          uint32_t o[32];
+          const int col0 = half * HD + c * 32;
+          ptx::tmem_ld32(lane_base + C::O_COL + col0, o);
+          ptx::tmem_ld_wait();
+          if (valid) {
+#pragma unroll
+            for (int v4 = 0; v4 < 8; ++v4)
+              *reinterpret_cast<uint4*>(po + col0 + v4 * 4) =
+                  make_uint4(o[v4 * 4], o[v4 * 4 + 1], o[v4 * 4 + 2], o[v4 * 4 + 3]);
+          }
+        }
+        if (valid && half == 0) P.text_ml[cur.part * 128 + row] = make_float2(m_run, l_run);
+      } else {
+        float rfac = 1.f;
+        const double* comp = nullptr;
+        if (P.rectify && valid) {
+          const int64_t n_blk = grow / g.B;
+          rfac = P.ws.r_eff[cur.h * g.N + n_blk];
+          comp = P.ws.comp + (cur.h * g.N + n_blk) * D;
+        }
+        const float inv_l = (count > 0 && l_run > 0.f) ? 1.f / l_run : 0.f;
+        __nv_bfloat16* orow = P.out + (cur.h * g.T + grow) * D;
+#pragma unroll
+        for (int c = 0; c < HD / 32; ++c) {
+          uint32_t o[32];
+          const int col0 = half * HD + c * 32;
+          ptx::tmem_ld32(lane_base + C::O_COL + col0, o);
+          ptx::tmem_ld_wait();
+          if (valid) {
+#pragma unroll
+            for (int v8 = 0; v8 < 4; ++v8) {
+              uint32_t w[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const int col = col0 + v8 * 8 + 2 * i;
+                float y0 = inv_l == 0.f ? 0.f : __uint_as_float(o[v8 * 8 + 2 * i]) * inv_l * rfac;
+                float y1 = inv_l == 0.f ? 0.f : __uint_as_float(o[v8 * 8 + 2 * i + 1]) * inv_l * rfac;
+                if (comp) {
+                  y0 += (float)comp[col];
+                  y1 += (float)comp[col + 1];
+                }
+                w[i] = ptx::pack_bf16(y0, y1);
+              }
+              ptx::st_stream(orow + col0 + v8 * 8, make_uint4(w[0], w[1], w[2], w[3]), once);
+            }
+          }
+        }
+        if (valid && half == 0 && P.lse)
+          P.lse[cur.h * g.T + grow] = l_run > 0.f ? (log2f(l_run) + m_run) * 0.69314718055994531f : -INFINITY;
+      }
+      // O is read: the next tile's PV_0 (after its P_0 below) may overwrite it
+      ptx::tc_fence_before();
+      gs += count;
+    }
+  }
+
+  __syncwarp();
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<C::TMEM_COLS>(tmem);
+  }
+}
+
 // Split-K text tiles: merge the chunks' (O_c, m_c, l_c) of every text query
 // row into the final row, O = sum_c 2^(m_c - m*) O_c / sum_c 2^(m_c - m*) l_c
 // (the online-softmax merge, kernel.py:120-145 semantics), plus the LSE.
@@ -606,6 +1013,43 @@ bool make_tmap_3d(CUtensorMap* tm, const void* ptr, int64_t dim0, int64_t dim1, 
   return r == CUDA_SUCCESS;
 }
 
+template <int D, int BKV>
+cudaError_t launch_persistent(const Geometry& g, const void* q, const void* k, const void* v, void* out,
+                              float* lse, const Workspace& ws, bool rectify, bool text, cudaStream_t st) {
+  using C = Cfg<D, BKV, true, false>;
+  CUtensorMap tk, tv;
+  if (!make_tmap_3d(&tk, k, g.d, g.T, g.H, BKV) || !make_tmap_3d(&tv, v, g.d, g.T, g.H, BKV))
+    return cudaErrorInvalidValue;
+  TcParams P{};
+  P.g = g;
+  P.ws = ws;
+  P.out = static_cast<__nv_bfloat16*>(out);
+  P.q = static_cast<const __nv_bfloat16*>(q);
+  P.lse = lse;
+  P.rectify = rectify ? 1 : 0;
+  P.text_tiles_per_head = text ? (g.Tt + 127) / 128 : 0;
+  P.text_chunks = text_chunks(g);
+  P.chunk_blocks = (g.M + P.text_chunks - 1) / P.text_chunks;
+  P.video_tiles_per_head = (g.N * g.B + 127) / 128;
+  P.tiles_per_head = P.text_tiles_per_head * P.text_chunks + P.video_tiles_per_head;
+  P.text_part = ws.text_part;
+  P.text_ml = reinterpret_cast<float2*>(ws.text_ml);
+  P.scale_log2 = (float)(1.4426950408889634 / sqrt((double)g.d));
+  auto kern = attn_tc_persistent_kernel<D, BKV>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t n_tiles = g.H * P.tiles_per_head;
+  kern<<<(unsigned)std::min<int64_t>(n_tiles, sms), kThreads, C::SMEM, st>>>(tk, tv, P, n_tiles);
+  e = cudaGetLastError();
+  if (e != cudaSuccess || P.text_tiles_per_head == 0) return e;
+  text_combine_kernel<D><<<(unsigned)(g.H * P.text_tiles_per_head), 256, 0, st>>>(
+      P.text_part, P.text_ml, P.out, lse, g, P.text_tiles_per_head, P.text_chunks);
+  return cudaGetLastError();
+}
+
 template <int D, int BKV, bool QTM, bool VT, int EMU>
 cudaError_t launch_cfg(const Geometry& g, const void* q, const void* k, const void* v, void* out, float* lse,
                        const Workspace& ws, bool rectify, bool text, cudaStream_t st) {
@@ -670,6 +1114,17 @@ cudaError_t launch_attn_tc(const Geometry& g, const void* q, const void* k, cons
   // RSA_TC_EMU=n: n of every 8 exp2 pairs on the FMA pipe (polynomial) instead of MUFU
   static const int emu = [] { const char* e = getenv("RSA_TC_EMU"); return e ? atoi(e) : 0; }();
   const int sel = (qtm ? 2 : 0) + (vt ? 1 : 0);
+  // RSA_TC_PERSIST=0: one CTA per tile (attn_tc_kernel, with the diagnostic modes)
+  static const int persist = [] { const char* e = getenv("RSA_TC_PERSIST"); return e ? atoi(e) : 1; }();
+  if (persist && qtm && !vt && emu == 0) {
+#define RSA_TC_P(DD, BB) \
+  if (g.d == DD && g.B == BB) return launch_persistent<DD, BB>(g, q, k, v, out, lse, ws, rectify, text, st);
+    RSA_TC_P(128, 128)
+    RSA_TC_P(128, 64)
+    RSA_TC_P(64, 128)
+    RSA_TC_P(64, 64)
+#undef RSA_TC_P
+  }
   if (qtm && !vt && g.d == 128 && g.B == 128 && emu == 1)
     return launch_cfg<128, 128, true, false, 1>(g, q, k, v, out, lse, ws, rectify, text, st);
   if (qtm && !vt && g.d == 128 && g.B == 128 && emu == 2)

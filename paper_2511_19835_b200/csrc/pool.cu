@@ -328,7 +328,10 @@ pool_bulk_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
     // pass 1: plain fp64 sums of this thread's column pair over its row phase,
     // plus the magnitude range (bf16 bits & 0x7FFF is monotonic in |x|)
     double a0 = 0.0, a1 = 0.0;
-    uint32_t bmax = 0, bmin = 0xFFFFu;
+    // packed 16x2 magnitude tracking: max of (bits & 0x7FFF); min over
+    // nonzero values through the key (mag + 0x7FFF) & 0x7FFF (0 -> 0x7FFF,
+    // x -> x - 1; no carry crosses the halves)
+    uint32_t pmax = 0, pmin = 0x7FFF7FFFu;
     const bool text_k = (it.seg == 1) && (it.blk >= g.N);
     double* raw_out = text_k ? ws.k_cat + (it.h * g.n_cols + g.N + (it.blk * g.B - g.Tv)) * D : nullptr;
 #pragma unroll 8
@@ -337,9 +340,9 @@ pool_bulk_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
       const float x0 = __uint_as_float(w << 16), x1 = __uint_as_float(w & 0xFFFF0000u);
       a0 += (double)x0;
       a1 += (double)x1;
-      const uint32_t m0 = w & 0x7FFFu, m1 = (w >> 16) & 0x7FFFu;
-      bmax = max(bmax, max(m0, m1));
-      bmin = min(bmin, min(m0 ? m0 : 0xFFFFu, m1 ? m1 : 0xFFFFu));
+      const uint32_t mag = w & 0x7FFF7FFFu;
+      pmax = __vmaxu2(pmax, mag);
+      pmin = __vminu2(pmin, (mag + 0x7FFF7FFFu) & 0x7FFF7FFFu);
       if (raw_out) {
         raw_out[r * D + 2 * word] = (double)x0;
         raw_out[r * D + 2 * word + 1] = (double)x1;
@@ -347,6 +350,9 @@ pool_bulk_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
     }
     s_part[rp * D + 2 * word] = a0;
     s_part[rp * D + 2 * word + 1] = a1;
+    uint32_t bmax = max(pmax & 0xFFFFu, pmax >> 16);
+    const uint32_t kmin = min(pmin & 0xFFFFu, pmin >> 16);
+    uint32_t bmin = kmin == 0x7FFFu ? 0xFFFFu : kmin + 1;   // 0xFFFF: no nonzero value
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       bmax = max(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));

@@ -27,25 +27,26 @@ for _ in range(2):
     nat.check(lib.rsa_forward(C.byref(shape), C.byref(conf), _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse),
                               _ptr(ws), _stream()))
 torch.cuda.synchronize()
-n_text = heads * 2
-tiles = n_text + heads * 928
+tph = 2 * 8 + 928   # per head: 2 text tiles x 8 split-K chunks, then 928 video tiles
+tiles = heads * tph
 ts = lse.view(torch.int64)[:tiles * 8].view(tiles, 8).cpu().numpy()
+is_vid = (np.arange(tiles) % tph) >= 16
 t0 = ts[:, 0].min()
 rel = (ts[:, :7] - t0) / 1e3  # us
-vid = rel[n_text:]
+vid = rel[is_vid]
 print("kernel span us", rel[:, 6].max())
 for name, a, b in [("setup", 0, 1), ("q->first mma (mma thread)", 1, 2), ("mma loop", 2, 3),
                    ("softmax end - mma end", 3, 4), ("epilogue", 4, 5), ("teardown wait", 5, 6), ("total", 0, 6)]:
     dd = vid[:, b] - vid[:, a]
     print(f"{name:28s} median {np.median(dd):8.2f} us  p90 {np.percentile(dd, 90):8.2f}")
-sm = ts[n_text:, 7]
-order = np.argsort(ts[n_text:, 0])
+tsv = ts[is_vid]
+sm = tsv[:, 7]
 # gap between consecutive CTAs on the same SM
 gaps = []
 for s_ in np.unique(sm)[:148]:
     idx = np.where(sm == s_)[0]
-    st = np.sort(ts[n_text + idx, 0])
-    en = np.sort(ts[n_text + idx, 6])
+    st = np.sort(tsv[idx, 0])
+    en = np.sort(tsv[idx, 6])
     if len(st) > 2:
         gaps.extend(((st[1:] - en[:-1]) / 1e3).tolist())
 print("launch gap between CTAs on one SM: median %.2f us p90 %.2f" % (np.median(gaps), np.percentile(gaps, 90)))
