@@ -23,6 +23,7 @@
 #include "rsa_internal.cuh"
 
 #include <cfloat>
+#include <cstdlib>
 
 namespace rsa {
 namespace {
@@ -163,6 +164,7 @@ struct SelectParams {
   int variant;
   double inv_sqrt_d;
   int p2;  // power of two >= M for the sort
+  int use_sort;  // 1: top-K from one full bitonic sort of the row (no radix select)
 };
 
 // (value desc, index asc) ordering == numpy argsort(-a, kind="stable")
@@ -258,9 +260,40 @@ __global__ void __launch_bounds__(RT) select_rows_kernel(SelectParams P) {
     // can only enlarge the count beyond K when the sequential cumsum of the
     // sorted top-K stays below p; only then is the full sort needed.
     const int64_t K = P.k_floor < M ? P.k_floor : M;
+    bool need_full_sort = P.use_sort != 0;
+    if (!need_full_sort) {
     uint64_t prefix = 0, pmask = 0;
     int remaining = (int)K;
-    for (int shift = 56; shift >= 0; shift -= 8) {
+    // skip the leading bytes every key shares (a_pool in [0, 1]: sign and
+    // high exponent bits agree) -- one dominant histogram bin otherwise
+    // serialises its shared-memory atomics
+    uint64_t k_and = ~0ull, k_or = 0ull;
+    for (int64_t m = threadIdx.x; m < M; m += RT) {
+      const uint64_t key = (uint64_t)__double_as_longlong(ap[m]);
+      k_and &= key;
+      k_or |= key;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      k_and &= __shfl_xor_sync(0xffffffffu, k_and, o);
+      k_or |= __shfl_xor_sync(0xffffffffu, k_or, o);
+    }
+    __shared__ unsigned long long s_and[RT / 32], s_or[RT / 32];
+    __shared__ int sh_done;
+    if (threadIdx.x % 32 == 0) { s_and[threadIdx.x / 32] = k_and; s_or[threadIdx.x / 32] = k_or; }
+    __syncthreads();
+    k_and = ~0ull;
+    k_or = 0ull;
+    for (int w = 0; w < RT / 32; ++w) { k_and &= s_and[w]; k_or |= s_or[w]; }
+    const uint64_t differ = k_and ^ k_or;
+    int top = 56;
+    while (top > 0 && ((differ >> top) & 0xFF) == 0) top -= 8;
+    if (top < 56) {
+      pmask = ~0ull << (top + 8);
+      prefix = k_and & pmask;
+    }
+    if (threadIdx.x == 0) sh_done = 0;
+    for (int shift = top; shift >= 0; shift -= 8) {
       for (int i = threadIdx.x; i < 256; i += RT) hist[i] = 0u;
       __syncthreads();
       for (int64_t m = threadIdx.x; m < M; m += RT) {
@@ -284,7 +317,13 @@ __global__ void __launch_bounds__(RT) select_rows_kernel(SelectParams P) {
           unsigned run = excl;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            if (run + c[i] >= (unsigned)remaining) { sh_digit = 255 - 8 * lane - i; sh_rem = remaining - (int)run; break; }
+            if (run + c[i] >= (unsigned)remaining) {
+              sh_digit = 255 - 8 * lane - i;
+              sh_rem = remaining - (int)run;
+              // the whole boundary bin is selected: no lower digit can matter
+              sh_done = (run + c[i] == (unsigned)remaining);
+              break;
+            }
             run += c[i];
           }
         }
@@ -293,22 +332,24 @@ __global__ void __launch_bounds__(RT) select_rows_kernel(SelectParams P) {
       prefix |= (uint64_t)sh_digit << shift;
       pmask |= (uint64_t)0xFF << shift;
       remaining = sh_rem;
+      if (sh_done) break;
     }
     {
       // keys > v* are in; the first `remaining` keys == v* (ascending index) too
       const int64_t chunk = (M + RT - 1) / RT;
       const int64_t lo = threadIdx.x * chunk, hi = min(lo + chunk, M);
       int eq = 0;
-      for (int64_t m = lo; m < hi; ++m) eq += (uint64_t)__double_as_longlong(ap[m]) == prefix;
+      // keys compared on the resolved digits only (all of them unless the
+      // boundary bin was taken whole, where ties below cannot matter)
+      for (int64_t m = lo; m < hi; ++m) eq += ((uint64_t)__double_as_longlong(ap[m]) & pmask) == prefix;
       int tot_eq;
       int rank = block_excl_scan(eq, scan_tmp, &tot_eq);
       for (int64_t m = lo; m < hi; ++m) {
-        const uint64_t key = (uint64_t)__double_as_longlong(ap[m]);
+        const uint64_t key = (uint64_t)__double_as_longlong(ap[m]) & pmask;
         if (key > prefix || (key == prefix && rank++ < remaining)) bits[m] = BIT_IMPORTANCE;
       }
     }
     __syncthreads();
-    bool need_full_sort = false;
     if (P.p > 0.0) {
       // sequential cumsum of the top-K in sorted order (masks.py:99): gather, sort, sum
       int kp2 = 1;
@@ -331,6 +372,7 @@ __global__ void __launch_bounds__(RT) select_rows_kernel(SelectParams P) {
       }
       __syncthreads();
       need_full_sort = sh_count != 0;
+    }
     }
     if (need_full_sort) {
       for (int i = threadIdx.x; i < P.p2; i += RT) {
@@ -504,6 +546,7 @@ cudaError_t launch_select(const Geometry& g, const rsa_config& cfg, int64_t k_fl
   int p2 = 1;
   while (p2 < g.M) p2 <<= 1;
   P.p2 = p2;
+  P.use_sort = 0;   // radix select (a full bitonic sort of every row measured 2x slower)
   const size_t smem = (size_t)(g.N + g.Tt) * 8 + (size_t)g.M * 8 + (size_t)p2 * 12 + (size_t)g.M + 16;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(select_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -303,3 +303,44 @@ def test_tcgen05_unrectified_block_sparse_seam():
                                         mask, grid, kernel="tcgen05")
     _, expected = O.masked_attention_fp64(qv, k, v, mask, O.kv_lengths(n, m, block, last), block)
     assert_bf16_close(out, expected, "seam")
+
+
+@pytest.mark.parametrize("block,d,n_q", [(64, 64, 150), (128, 128, 140)])
+def test_tcgen05_split_k_text_chunks(block, d, n_q):
+    """M > 128 kv blocks: every 128-row text tile of the tensor-core kernel is
+    split into kv-block chunks whose partial (O, max, sum) text_combine_kernel
+    merges.  Against the CUDA-core kernel and the fp32 oracle."""
+    t_v, t_t = block * n_q, 200
+    qv, qt, k, v = O.gen_synthetic(7, t_v, t_t, d, block, (1, 1, t_v), 1.0, 2.0, 0.3)
+    qv, qt, k, v = (O.round_to_bf16(x) for x in (qv, qt, k, v))
+    q = torch.cat([to_bf16_tensor(qv), to_bf16_tensor(qt)])[None]
+    kk, vv = to_bf16_tensor(k)[None], to_bf16_tensor(v)[None]
+    outs = {}
+    for kern in ("tcgen05", "simt"):
+        lse = torch.empty(1, t_v + t_t, dtype=torch.float32, device="cuda")
+        outs[kern] = (rsa.rectified_sparse_attention(q, kk, vv, num_text_tokens=t_t, block=block,
+                                                     top_k_fraction=0.1, kernel=kern, lse=lse,
+                                                     check_status=True)[0], lse[0])
+    text = slice(t_v, t_v + t_t)
+    diff = (outs["tcgen05"][0][text].float() - outs["simt"][0][text].float()).abs().max().item()
+    assert diff <= 1e-2, diff
+    lse_diff = (outs["tcgen05"][1][text] - outs["simt"][1][text]).abs().max().item()
+    assert lse_diff <= 1e-2, lse_diff
+    ref = O.pipeline(qv, qt, k, v, block, 0.1, 0.0, 0, False, "sparse-rectified")
+    assert_bf16_close(outs["tcgen05"][0], np.concatenate([ref["o_video"], ref["o_text"]]), "split-K")
+
+
+def test_forward_from_host_tensors_matches_device():
+    """The end-to-end call on host tensors (rsa_forward_host: H2D, K1-K3, D2H
+    pipelined over head chunks) returns exactly the device call's output."""
+    heads, t_v, t_t, d, block = 3, 64 * 30, 100, 64, 64
+    g = torch.Generator().manual_seed(3)
+    q, k, v = (torch.randn(1, heads, t_v + t_t, d, generator=g).to(torch.bfloat16) for _ in range(3))
+    want = rsa.rectified_sparse_attention(q.cuda(), k.cuda(), v.cuda(), num_text_tokens=t_t, block=block,
+                                          top_k_fraction=0.2).cpu()
+    for pinned, chunk in ((True, 1), (True, 2), (False, 3)):
+        args = [x.pin_memory() if pinned else x for x in (q, k, v)]
+        got = rsa.rectified_sparse_attention(*args, num_text_tokens=t_t, block=block, top_k_fraction=0.2,
+                                             heads_per_chunk=chunk)
+        assert not got.is_cuda
+        assert torch.equal(got, want), (pinned, chunk)
