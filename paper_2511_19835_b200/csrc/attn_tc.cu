@@ -774,7 +774,7 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid
           for (int i = 0; i < 32; ++i) mx4[i & 3] = fmaxf(mx4[i & 3], __uint_as_float(sr[c][i]));
         float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
         red_max[(gj & 1) * 256 + half * 128 + row] = mx;
-        asm volatile("bar.sync 1, 256;" ::: "memory");
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + quad) : "memory");   // the quad's two warps only
         mx = fmaxf(mx, red_max[(gj & 1) * 256 + (half ^ 1) * 128 + row]);
         const float m_blk = mx * sl2;              // -inf if the row retains nothing here
         const float m_old = m_run;
@@ -834,7 +834,7 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid
 
       // ---- epilogue: O / l, rectification (rectify.py:66-89), bf16 store, LSE ----
       red_max[512 + half * 128 + row] = l_part;
-      asm volatile("bar.sync 1, 256;" ::: "memory");
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + quad) : "memory");   // the quad's two warps only
       const float l_run = l_part + red_max[512 + (half ^ 1) * 128 + row];
       if (count > 0) {
         ptx::mbar_wait(pv_done, (uint32_t)((gs + count - 1) & 1));

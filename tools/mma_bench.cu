@@ -94,7 +94,80 @@ void run(const char* name, int sms) {
   cudaFree(d);
 }
 
+
+// The attention kernel's per-step MMA sequence: 8 x S = Q K^T (TS, A = Q in
+// TMEM, B = K K-major, N = 128) into S buffer j%2 + 2 commits, then 8 x
+// O += P V (TS, A = P in S buffer (j-1)%2, B = V MN-major or V^T K-major,
+// N = D = 128) + 2 commits.  Cycles per step (ideal 16 x 64 = 1024).
+template <bool VT, bool COMMITS>
+__global__ void __launch_bounds__(128, 1) step_bench(long long* out, int steps) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint32_t slot;
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t dummy[4];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x / 32;
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); for (int i = 0; i < 4; ++i) mbar_init(dummy + i, 1); fence_barrier_init(); }
+  if (warp == 0) tmem_alloc<512>(&slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  constexpr uint32_t IDS = idesc_bf16(128, 128, false);
+  constexpr uint32_t IDO = idesc_bf16(128, 128, !VT);
+  if (warp == 1) {
+    const uint32_t kb = __shfl_sync(0xffffffffu, smem_u32(base), 0);
+    const uint32_t vb = kb + 32768;
+    long long t0 = clock64();
+    for (int j = 0; j < steps; ++j) {
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          mma_ts(tmem + (j & 1) * 128, tmem + 384 + k * 8, sw128_desc(kb + (k / 4) * 16384 + (k % 4) * 32, 16, 1024), IDS, k > 0);
+        if (COMMITS) { tc_commit(dummy + 0); tc_commit(dummy + 1); }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint64_t b = VT ? sw128_desc(vb + (k / 4) * 16384 + (k % 4) * 32, 16, 1024)
+                                : sw128_desc(vb + k * 2048, 16384, 1024);
+          mma_ts(tmem + 256, tmem + ((j + 1) & 1) * 128 + k * 8, b, IDO, 1);
+        }
+        if (COMMITS) { tc_commit(dummy + 2); tc_commit(dummy + 3); }
+      }
+      __syncwarp();
+    }
+    if (elect_one()) tc_commit(&bar);
+    __syncwarp();
+    mbar_wait(&bar, 0);
+    if (threadIdx.x == 32) out[blockIdx.x] = clock64() - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) { tc_fence_after(); tmem_dealloc<512>(tmem); }
+}
+
+template <bool VT, bool COMMITS>
+void run_step(const char* name) {
+  long long* d;
+  const int sms = 148, steps = 2048;
+  cudaMalloc(&d, sms * sizeof(long long));
+  auto k = step_bench<VT, COMMITS>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  k<<<sms, 128, 100 * 1024>>>(d, steps);
+  k<<<sms, 128, 100 * 1024>>>(d, steps);
+  long long h[148];
+  cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  double avg = 0;
+  for (int i = 0; i < sms; ++i) avg += h[i];
+  printf("%-34s cycles/step %7.1f (ideal 1024)  err=%s\n", name, avg / sms / steps,
+         cudaGetErrorString(cudaGetLastError()));
+  cudaFree(d);
+}
+
 int main() {
+  run_step<false, true>("kernel step: V MN-major + commits");
+  run_step<true, true>("kernel step: V^T K-major + commits");
+  run_step<false, false>("kernel step: V MN-major, no commits");
+  run_step<true, false>("kernel step: V^T K-major, no commits");
   int sms = 148;
   run<128, false, 1>("SS N=128", sms);
   run<128, true, 1>("TS N=128", sms);
