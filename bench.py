@@ -67,6 +67,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-blocks", type=int, default=96)
     ap.add_argument("--profile", action="store_true", help="fewer steps, no side legs (for ncu)")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="gloo: plumbing check of the multi-rank path (ranks may share one GPU)")
     ap.add_argument("--input-layout", choices=["heads", "seq"], default="heads",
                     help="heads: inputs head-sharded (no collective); seq: video tokens sequence-"
                          "sharded, Ulysses NCCL all-to-all before/after the pipeline (N>1)")
@@ -191,7 +193,16 @@ def cpu_reference_sample(cfg, f, variant, sample_blocks, seed=42):
     head's text queries; extrapolate to the whole call."""
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     import numpy as np
+    from threadpoolctl import threadpool_limits
     from oracle import rsa_oracle as O
+    # single-threaded BLAS inside the oracle's per-query-block thread pool (all
+    # host cores): numpy may already have started multi-threaded OpenBLAS when
+    # torch was imported, which oversubscribes the cores 16x
+    with threadpool_limits(limits=1, user_api="blas"):
+        return _cpu_reference_sample(np, O, cfg, f, variant, sample_blocks, seed)
+
+
+def _cpu_reference_sample(np, O, cfg, f, variant, sample_blocks, seed):
     t_v, t_t, d, B = cfg["t_v"], cfg["t_t"], cfg["d"], cfg["block"]
     if t_t:
         qv, qt, k, v = O.gen_synthetic(seed, t_v, t_t, d, B, cfg["grid"], 1.0, 2.0, 0.3)
@@ -271,10 +282,14 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local % max(1, torch.cuda.device_count())   # --dist-backend gloo smoke runs share one GPU
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
     cfg = CONFIGS[args.config]
     f = 1.0 - args.sparsity
     # head sharding: rank r owns heads [lo, hi)
