@@ -169,6 +169,34 @@ rsa_status rsa_text_full_attention(int64_t heads, int64_t n_queries, int64_t n_k
                                    const void* k, const void* v, void* out, float* lse,
                                    void* workspace, void* stream);
 
+/* Morton (Z-order) token permutation of a (t, h, w) grid, w fastest
+ * (core.py:263-291 morton_code_3d / morton_permutation): perm[i] = original
+ * video row placed at position i (numpy's stable argsort of the codes).
+ * `perm` is HOST memory of t*h*w entries; no device work. */
+rsa_status rsa_morton_permutation(int64_t t, int64_t h, int64_t w, int32_t* perm);
+
+/* Row permutation of one [heads][T][d] tensor of `shape`'s dtype (the data
+ * movement of reorder_morton, core.py:294-318): video rows dst[r] =
+ * src[perm[r]], or dst[perm[r]] = src[r] with `inverse` (undo); text rows are
+ * copied.  `perm` is a DEVICE int32 array of t_video entries. */
+rsa_status rsa_permute_rows(const rsa_shape* shape, const int32_t* perm, const void* src, void* dst,
+                            int32_t inverse, void* stream);
+
+/* Bytes of the `perm_buf` rsa_forward_permuted needs (permuted K and V). */
+size_t rsa_permuted_buffer_size(const rsa_shape* shape);
+
+/* rsa_forward on the problem whose video tokens are reordered by `perm`
+ * (DEVICE int32 [t_video]) -- the reference harness's morton_reorder option,
+ * reorder_morton + rectified_attention_pipeline (harness.py:172-173) -- with
+ * Q/K/V and O/LSE in the ORIGINAL token order: K1 gathers the rows and writes
+ * the permuted K/V into `perm_buf`, K3 gathers the query rows and scatters the
+ * output rows; the workspace results (masks, a_pool, ...) are those of the
+ * reordered problem.  bf16 with the tcgen05 kernel only (RSA_ERR_UNSUPPORTED
+ * otherwise: use rsa_permute_rows + rsa_forward). */
+rsa_status rsa_forward_permuted(const rsa_shape* shape, const rsa_config* cfg, const void* q,
+                                const void* k, const void* v, const int32_t* perm, void* perm_buf,
+                                void* out, float* lse, void* workspace, void* stream);
+
 /* Synchronises `stream` and converts device-side status flags (e.g. a
  * reallocation denominator <= 0, ipar.py:62-64) into an rsa_status. */
 rsa_status rsa_check_device_status(void* workspace, void* stream);

@@ -19,6 +19,7 @@ __version__ = "0.1.0"
 
 _LAZY = {"rectified_attention_pipeline", "block_sparse_attention", "text_full_attention",
          "rectified_sparse_attention"}
+_REORDER = {"morton_permutation", "reorder_morton", "inverse_permutation"}
 
 
 def __getattr__(name):
@@ -26,4 +27,7 @@ def __getattr__(name):
     if name in _LAZY:
         from . import pipeline
         return getattr(pipeline, name)
+    if name in _REORDER:
+        from . import reorder
+        return getattr(reorder, name)
     raise AttributeError(name)

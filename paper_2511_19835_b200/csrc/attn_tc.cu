@@ -67,6 +67,7 @@ struct TcParams {
   __nv_bfloat16* out;
   const __nv_bfloat16* q;
   float* lse;
+  const int32_t* perm;   // token permutation (video row r = original row perm[r]) or null
   float* text_part;   // [H][text tiles][chunks][128][D] unnormalised partial O
   float2* text_ml;    // [H][text tiles][chunks][128] (row max log2, row sum)
   int rectify;
@@ -715,7 +716,9 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid
     auto store_q = [&](const TileDesc& t) {
       uint32_t qw[QW];
       const int64_t grow = t.q_row0 + row;
-      const uint4* src = reinterpret_cast<const uint4*>(P.q + (t.h * g.T + grow) * D + half * (D / 2));
+      // permuted problem: gather the query row from its original position
+      const int64_t srow = (P.perm && grow < g.Tv) ? P.perm[grow] : grow;
+      const uint4* src = reinterpret_cast<const uint4*>(P.q + (t.h * g.T + srow) * D + half * (D / 2));
 #pragma unroll
       for (int i = 0; i < QW / 4; ++i) {
         const uint4 x = grow < g.T ? ptx::ld_stream(src + i, once) : make_uint4(0, 0, 0, 0);
@@ -868,7 +871,9 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid
           comp = P.ws.comp + (cur.h * g.N + n_blk) * D;
         }
         const float inv_l = (count > 0 && l_run > 0.f) ? 1.f / l_run : 0.f;
-        __nv_bfloat16* orow = P.out + (cur.h * g.T + grow) * D;
+        // permuted problem: scatter the row back to its original position
+        const int64_t orig = (P.perm && valid) ? P.perm[grow] : grow;
+        __nv_bfloat16* orow = P.out + (cur.h * g.T + orig) * D;
 #pragma unroll
         for (int c = 0; c < HD / 32; ++c) {
           uint32_t o[32];
@@ -895,7 +900,7 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid
           }
         }
         if (valid && half == 0 && P.lse)
-          P.lse[cur.h * g.T + grow] = l_run > 0.f ? (log2f(l_run) + m_run) * 0.69314718055994531f : -INFINITY;
+          P.lse[cur.h * g.T + orig] = l_run > 0.f ? (log2f(l_run) + m_run) * 0.69314718055994531f : -INFINITY;
       }
       // O is read: the next tile's PV_0 (after its P_0 below) may overwrite it
       ptx::tc_fence_before();
@@ -1015,7 +1020,8 @@ bool make_tmap_3d(CUtensorMap* tm, const void* ptr, int64_t dim0, int64_t dim1, 
 
 template <int D, int BKV>
 cudaError_t launch_persistent(const Geometry& g, const void* q, const void* k, const void* v, void* out,
-                              float* lse, const Workspace& ws, bool rectify, bool text, cudaStream_t st) {
+                              float* lse, const Workspace& ws, bool rectify, bool text, cudaStream_t st,
+                              const int32_t* perm) {
   using C = Cfg<D, BKV, true, false>;
   CUtensorMap tk, tv;
   if (!make_tmap_3d(&tk, k, g.d, g.T, g.H, BKV) || !make_tmap_3d(&tv, v, g.d, g.T, g.H, BKV))
@@ -1026,6 +1032,7 @@ cudaError_t launch_persistent(const Geometry& g, const void* q, const void* k, c
   P.out = static_cast<__nv_bfloat16*>(out);
   P.q = static_cast<const __nv_bfloat16*>(q);
   P.lse = lse;
+  P.perm = perm;
   P.rectify = rectify ? 1 : 0;
   P.text_tiles_per_head = text ? (g.Tt + 127) / 128 : 0;
   P.text_chunks = text_chunks(g);
@@ -1104,7 +1111,8 @@ bool tc_supported(const Geometry& g) {
 }
 
 cudaError_t launch_attn_tc(const Geometry& g, const void* q, const void* k, const void* v, void* out, float* lse,
-                           const Workspace& ws, bool rectify, bool text, cudaStream_t st, int* launches) {
+                           const Workspace& ws, bool rectify, bool text, cudaStream_t st, int* launches,
+                           const int32_t* perm) {
   static const bool vt_on = [] { const char* e = getenv("RSA_TC_VT"); return e && atoi(e) != 0; }();
   *launches += (vt_on ? 2 : 1) + (text && g.Tt > 0 ? 1 : 0);   // (V transpose) + attention (+ text combine)
   // Variant knobs (profiling): RSA_TC_QTMEM=1 keeps Q in TMEM (2 S buffers);
@@ -1118,13 +1126,14 @@ cudaError_t launch_attn_tc(const Geometry& g, const void* q, const void* k, cons
   static const int persist = [] { const char* e = getenv("RSA_TC_PERSIST"); return e ? atoi(e) : 1; }();
   if (persist && qtm && !vt && emu == 0) {
 #define RSA_TC_P(DD, BB) \
-  if (g.d == DD && g.B == BB) return launch_persistent<DD, BB>(g, q, k, v, out, lse, ws, rectify, text, st);
+  if (g.d == DD && g.B == BB) return launch_persistent<DD, BB>(g, q, k, v, out, lse, ws, rectify, text, st, perm);
     RSA_TC_P(128, 128)
     RSA_TC_P(128, 64)
     RSA_TC_P(64, 128)
     RSA_TC_P(64, 64)
 #undef RSA_TC_P
   }
+  if (perm) return cudaErrorNotSupported;   // the permuted problem runs on the persistent kernel only
   if (qtm && !vt && g.d == 128 && g.B == 128 && emu == 1)
     return launch_cfg<128, 128, true, false, 1>(g, q, k, v, out, lse, ws, rectify, text, st);
   if (qtm && !vt && g.d == 128 && g.B == 128 && emu == 2)

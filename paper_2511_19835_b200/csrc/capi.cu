@@ -146,7 +146,7 @@ bool use_tc(const rsa_shape* s, const rsa::Geometry& g) {
 
 rsa_status run_attention(const rsa_shape* s, const rsa::Geometry& g, const rsa::Workspace& ws,
                          const void* q, const void* k, const void* v, void* out, float* lse,
-                         bool rectify, bool text, cudaStream_t st) {
+                         bool rectify, bool text, cudaStream_t st, const int32_t* perm = nullptr) {
   cudaError_t e;
   const bool tc = use_tc(s, g);
   if (s->kernel == RSA_KERNEL_TCGEN05 && !tc)
@@ -154,9 +154,10 @@ rsa_status run_attention(const rsa_shape* s, const rsa::Geometry& g, const rsa::
   if (tc) {
     e = rsa::launch_tile_lists(g, ws, st, &g_launches);
     if (e != cudaSuccess) return cuda_fail(e, "tile_lists");
-    e = rsa::launch_attn_tc(g, q, k, v, out, lse, ws, rectify, text, st, &g_launches);
+    e = rsa::launch_attn_tc(g, q, k, v, out, lse, ws, rectify, text, st, &g_launches, perm);
     if (e != cudaSuccess) return cuda_fail(e, "attn_tc");
   } else {
+    if (perm) return fail(RSA_ERR_UNSUPPORTED, "the permuted problem needs the tcgen05 kernel (bf16)");
     e = rsa::launch_attn_simt(g, q, k, v, out, lse, ws, rectify, false, st, &g_launches);
     if (e != cudaSuccess) return cuda_fail(e, "attn_simt(video)");
     if (text && g.Tt > 0) {
@@ -373,6 +374,63 @@ rsa_status rsa_text_full_attention(int64_t heads, int64_t n_queries, int64_t n_k
                                         static_cast<cudaStream_t>(stream), &g_launches);
   if (e != cudaSuccess) return cuda_fail(e, "attn_simt(text)");
   return RSA_OK;
+}
+
+rsa_status rsa_morton_permutation(int64_t t, int64_t h, int64_t w, int32_t* perm) {
+  if (t < 1 || h < 1 || w < 1 || t >= (1 << 21) || h >= (1 << 21) || w >= (1 << 21))
+    return fail(RSA_ERR_SHAPE, "grid_dims must be positive and < 2^21 each");
+  if (t * h * w >= ((int64_t)1 << 31)) return fail(RSA_ERR_UNSUPPORTED, "more than 2^31 tokens");
+  if (!perm) return fail(RSA_ERR_SHAPE, "null pointer");
+  rsa::morton_permutation_host(t, h, w, perm);
+  return RSA_OK;
+}
+
+rsa_status rsa_permute_rows(const rsa_shape* shape, const int32_t* perm, const void* src, void* dst,
+                            int32_t inverse, void* stream) {
+  rsa::Geometry g;
+  rsa_status s = make_geometry(shape, &g);
+  if (s != RSA_OK) return s;
+  if (!perm || !src || !dst) return fail(RSA_ERR_SHAPE, "null pointer");
+  if (src == dst) return fail(RSA_ERR_SHAPE, "rsa_permute_rows cannot run in place");
+  cudaError_t e = rsa::launch_permute_rows(g, perm, src, dst, inverse != 0, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "permute_rows");
+  return RSA_OK;
+}
+
+size_t rsa_permuted_buffer_size(const rsa_shape* shape) {
+  rsa::Geometry g;
+  if (make_geometry(shape, &g) != RSA_OK) return 0;
+  const size_t esz = g.dtype == RSA_BF16 ? 2 : g.dtype == RSA_F32 ? 4 : 8;
+  return 2 * (size_t)g.H * g.T * g.d * esz;   // permuted K and V
+}
+
+rsa_status rsa_forward_permuted(const rsa_shape* shape, const rsa_config* cfg, const void* q, const void* k,
+                                const void* v, const int32_t* perm, void* perm_buf, void* out, float* lse,
+                                void* workspace, void* stream) {
+  g_launches = 0;
+  rsa::Geometry g;
+  rsa_status s = make_geometry(shape, &g);
+  if (s != RSA_OK) return s;
+  s = check_config(cfg);
+  if (s != RSA_OK) return s;
+  if (!q || !k || !v || !perm || !perm_buf || !out || !workspace) return fail(RSA_ERR_SHAPE, "null pointer");
+  if (!use_tc(shape, g)) return fail(RSA_ERR_UNSUPPORTED, "the fused permuted path needs bf16 and the tcgen05 kernel");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  rsa::Workspace ws = bind(g, workspace);
+  char* kp = static_cast<char*>(perm_buf);
+  char* vp = kp + (size_t)g.H * g.T * g.d * 2;
+  cudaError_t e = cudaMemsetAsync(ws.status, 0, 64, st);
+  if (e != cudaSuccess) return cuda_fail(e, "memset status");
+  // K1: gathers the video rows in permuted order, writes permuted K and V
+  e = rsa::launch_pool(g, q, k, v, ws, st, &g_launches, perm, kp, vp);
+  if (e == cudaErrorNotSupported)
+    return fail(RSA_ERR_UNSUPPORTED, "the fused permuted path needs 16-byte aligned bf16 rows, d in {64, 128}");
+  if (e != cudaSuccess) return cuda_fail(e, "pool(permuted)");
+  const int64_t k_floor = (int64_t)std::ceil(cfg->top_k_fraction * (double)g.M);
+  e = rsa::launch_select(g, *cfg, k_floor, ws, st, &g_launches);
+  if (e != cudaSuccess) return cuda_fail(e, "select");
+  // K3 on the permuted K/V; Q rows gathered and O / LSE rows scattered via perm
+  return run_attention(shape, g, ws, q, kp, vp, out, lse, rectifies(cfg->variant), true, st, perm);
 }
 
 rsa_status rsa_check_device_status(void* workspace, void* stream) {

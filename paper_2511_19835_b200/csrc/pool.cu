@@ -284,7 +284,8 @@ __device__ __forceinline__ PoolItem pool_item(const Geometry& g, int64_t i) {
 template <int D, int STAGES>
 __global__ void __launch_bounds__(kBulkThreads, 2)
 pool_bulk_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k,
-                 const __nv_bfloat16* __restrict__ v, Workspace ws, Geometry g, int64_t n_items) {
+                 const __nv_bfloat16* __restrict__ v, Workspace ws, Geometry g, int64_t n_items,
+                 const int32_t* __restrict__ perm, __nv_bfloat16* kp, __nv_bfloat16* vp) {
   constexpr int WPR = D / 2;                   // 32-bit words (bf16 pairs) per row
   constexpr int RP = kBulkThreads / WPR;       // row phases
   extern __shared__ __align__(128) uint8_t smem[];
@@ -308,14 +309,31 @@ pool_bulk_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (t == 0) {
+  // Stage item i into ring slot s (warp 0).  With a token permutation `perm`
+  // (video row r of the permuted problem = original row perm[r]) a video
+  // block is gathered row by row, 4 rows per lane; text blocks and the
+  // identity order are one contiguous copy.
+  auto fetch = [&](int64_t i, int s) {
+    const PoolItem it = pool_item(g, i);
+    uint32_t bytes;
+    const void* src = src_of(it, bytes);
+    uint8_t* dst = ring + s * stage_bytes;
+    if (perm && it.blk < g.N) {
+      if (t == 0) bar_expect_tx(full + s, bytes);
+      __syncwarp();
+      const __nv_bfloat16* base = it.seg == 0 ? q : it.seg == 1 ? k : v;
+      for (int r = t; r < g.B; r += 32)
+        bulk_g2s(dst + r * D * 2, base + (it.h * g.T + perm[it.blk * g.B + r]) * D, D * 2, full + s);
+    } else if (t == 0) {
+      bar_expect_tx(full + s, bytes);
+      bulk_g2s(dst, src, bytes, full + s);
+    }
+  };
+  if (t < 32) {
     for (int s = 0; s < STAGES; ++s) {
       const int64_t i = blockIdx.x + (int64_t)s * gridDim.x;
       if (i >= n_items) break;
-      uint32_t bytes;
-      const void* src = src_of(pool_item(g, i), bytes);
-      bar_expect_tx(full + s, bytes);
-      bulk_g2s(ring + s * stage_bytes, src, bytes, full + s);
+      fetch(i, s);
     }
   }
   int64_t kk = 0;
@@ -325,6 +343,14 @@ pool_bulk_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
     const int64_t len = (it.blk < g.N) ? g.B : (it.blk == g.M - 1 ? g.last_len : g.B);
     bar_wait(full + s, (uint32_t)((kk / STAGES) & 1));
     const uint32_t* blk = reinterpret_cast<const uint32_t*>(ring + s * stage_bytes);
+    if (kp && it.seg > 0 && t == 0) {
+      // the permuted K / V block, contiguous, for K3's TMA (shared -> global bulk copy)
+      __nv_bfloat16* dstp = (it.seg == 1 ? kp : vp) + (it.h * g.T + it.blk * g.B) * D;
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n\t"
+                   "cp.async.bulk.commit_group;" ::"l"(dstp),
+                   "r"((uint32_t)__cvta_generic_to_shared(blk)), "r"((uint32_t)(len * D * 2))
+                   : "memory");
+    }
     // pass 1: plain fp64 sums of this thread's column pair over its row phase,
     // plus the magnitude range (bf16 bits & 0x7FFF is monotonic in |x|)
     double a0 = 0.0, a1 = 0.0;
@@ -392,15 +418,13 @@ pool_bulk_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
       s_part[RP * D + rp * D + 2 * word + 1] = l1;
       __syncthreads();
     }
-    // stage s is free: refill it with this CTA's item STAGES ahead
-    if (t == 0) {
+    // stage s is free (its permuted copy, if any, has been read out): refill
+    // it with this CTA's item STAGES ahead
+    if (t < 32) {
+      if (t == 0 && kp) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      __syncwarp();
       const int64_t nx = i + (int64_t)STAGES * gridDim.x;
-      if (nx < n_items) {
-        uint32_t bytes;
-        const void* src = src_of(pool_item(g, nx), bytes);
-        bar_expect_tx(full + s, bytes);
-        bulk_g2s(ring + s * stage_bytes, src, bytes, full + s);
-      }
+      if (nx < n_items) fetch(nx, s);
     }
     for (int col = t; col < D; col += kBulkThreads) {
       double sum;
@@ -434,11 +458,12 @@ pool_bulk_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
     }
     __syncthreads();
   }
+  if (t == 0 && kp) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 template <int D>
 cudaError_t launch_bulk(const Geometry& g, const void* q, const void* k, const void* v, const Workspace& ws,
-                        cudaStream_t st) {
+                        cudaStream_t st, const int32_t* perm, void* kp, void* vp) {
   constexpr int STAGES = 3;
   constexpr int RP = kBulkThreads / (D / 2);
   const size_t smem = (size_t)STAGES * g.B * D * 2 + STAGES * 8 + 2 * RP * D * 8 + 64;
@@ -451,7 +476,8 @@ cudaError_t launch_bulk(const Geometry& g, const void* q, const void* k, const v
   const int64_t n_items = g.H * (g.N + 2 * g.M);
   const int64_t grid = std::min<int64_t>(n_items, (int64_t)sms * 2);
   kern<<<(unsigned)grid, kBulkThreads, smem, st>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
-                                                   (const __nv_bfloat16*)v, ws, g, n_items);
+                                                   (const __nv_bfloat16*)v, ws, g, n_items, perm,
+                                                   (__nv_bfloat16*)kp, (__nv_bfloat16*)vp);
   return cudaGetLastError();
 }
 
@@ -473,7 +499,8 @@ cudaError_t launch_typed(const Geometry& g, const void* q, const void* k, const 
 }  // namespace
 
 cudaError_t launch_pool(const Geometry& g, const void* q, const void* k, const void* v,
-                        const Workspace& ws, cudaStream_t st, int* launches) {
+                        const Workspace& ws, cudaStream_t st, int* launches, const int32_t* perm,
+                        void* kp, void* vp) {
   ++*launches;
   switch (g.dtype) {
     case RSA_BF16: {
@@ -481,12 +508,13 @@ cudaError_t launch_pool(const Geometry& g, const void* q, const void* k, const v
       // that fits three ring stages per CTA, two CTAs per SM
       const bool aligned = ((uintptr_t)q % 16 == 0) && ((uintptr_t)k % 16 == 0) && ((uintptr_t)v % 16 == 0);
       const bool fits = g.B * g.d * 2 * 3 <= 96 * 1024;
-      if (aligned && fits && g.d == 128) return launch_bulk<128>(g, q, k, v, ws, st);
-      if (aligned && fits && g.d == 64) return launch_bulk<64>(g, q, k, v, ws, st);
+      if (aligned && fits && g.d == 128) return launch_bulk<128>(g, q, k, v, ws, st, perm, kp, vp);
+      if (aligned && fits && g.d == 64) return launch_bulk<64>(g, q, k, v, ws, st, perm, kp, vp);
+      if (perm) return cudaErrorNotSupported;
       return launch_typed<__nv_bfloat16>(g, q, k, v, ws, st);
     }
-    case RSA_F32: return launch_typed<float>(g, q, k, v, ws, st);
-    default: return launch_typed<double>(g, q, k, v, ws, st);
+    case RSA_F32: if (perm) return cudaErrorNotSupported; return launch_typed<float>(g, q, k, v, ws, st);
+    default: if (perm) return cudaErrorNotSupported; return launch_typed<double>(g, q, k, v, ws, st);
   }
 }
 

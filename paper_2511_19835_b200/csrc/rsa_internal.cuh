@@ -71,8 +71,12 @@ template <> __device__ __forceinline__ float from_acc<float>(float x) { return x
 template <typename T> __device__ __forceinline__ T from_acc(double x) { return (T)x; }
 
 // ---- launchers (one per .cu file) -----------------------------------------
+// perm (device int32 [T_v], may be null): pool the video tokens in the order
+// perm (row r of the permuted problem = original row perm[r]) and write the
+// permuted K and V ([H][T][d], text rows copied) to kp / vp for K3
 cudaError_t launch_pool(const Geometry& g, const void* q, const void* k, const void* v,
-                        const Workspace& ws, cudaStream_t st, int* launches);
+                        const Workspace& ws, cudaStream_t st, int* launches,
+                        const int32_t* perm = nullptr, void* kp = nullptr, void* vp = nullptr);
 cudaError_t launch_select(const Geometry& g, const rsa_config& cfg, int64_t k_floor,
                           const Workspace& ws, cudaStream_t st, int* launches);
 cudaError_t launch_lists_from_mask(const Geometry& g, const uint8_t* mask,
@@ -83,8 +87,11 @@ cudaError_t launch_attn_simt(const Geometry& g, const void* q, const void* k, co
                              void* out, float* lse, const Workspace& ws, bool rectify,
                              bool text, cudaStream_t st, int* launches);
 bool tc_supported(const Geometry& g);
+void morton_permutation_host(int64_t t, int64_t h, int64_t w, int32_t* perm);
+cudaError_t launch_permute_rows(const Geometry& g, const int32_t* perm, const void* src, void* dst,
+                                bool inverse, cudaStream_t st);
 cudaError_t launch_attn_tc(const Geometry& g, const void* q, const void* k, const void* v,
                            void* out, float* lse, const Workspace& ws, bool rectify,
-                           bool text, cudaStream_t st, int* launches);
+                           bool text, cudaStream_t st, int* launches, const int32_t* perm = nullptr);
 
 }  // namespace rsa

@@ -237,14 +237,20 @@ def rectified_sparse_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor
                                variant: str = "sparse-rectified", sparsity: float | None = None,
                                kernel: str = "auto", lse: torch.Tensor | None = None,
                                workspace: torch.Tensor | None = None,
-                               check_status: bool = False, heads_per_chunk: int = 1) -> torch.Tensor:
+                               check_status: bool = False, heads_per_chunk: int = 1,
+                               grid_dims: tuple | None = None, morton: bool = False) -> torch.Tensor:
     """Rectified block-sparse attention for every (batch, head) of q/k/v
     ([..., T, d], the last ``num_text_tokens`` rows text).  ``sparsity=s`` is
     shorthand for top_k_fraction = 1 - s with p = 0, r = 0, no forced text.
     CUDA tensors: stream-ordered, no host synchronisation unless
     ``check_status``.  Host tensors (the end-to-end call): the copies in and
     out are pipelined with the compute over chunks of ``heads_per_chunk``
-    heads (rsa_forward_host) and the host output is returned."""
+    heads (rsa_forward_host) and the host output is returned.
+    ``morton=True`` (needs ``grid_dims`` = (t, h, w) of the video tokens):
+    the pipeline runs on the Morton-reordered problem, as the reference
+    harness's ``morton_reorder`` option does (harness.py:172-173), with the
+    gather fused into K1 and the scatter into the K3 epilogue -- inputs and
+    output stay in the original token order."""
     if sparsity is not None:
         top_k_fraction, weight_threshold, adjacency_radius, force_text_blocks = 1.0 - sparsity, 0.0, 0, False
     if top_k_fraction is None:
@@ -259,10 +265,24 @@ def rectified_sparse_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor
     cfg = nat.make_config(top_k_fraction, weight_threshold, adjacency_radius, force_text_blocks, variant)
     nat.plan(shape, cfg)
     if not q.is_cuda:
+        if morton:
+            raise ShapeError("morton=True needs CUDA tensors (use reorder_morton for host arrays)")
         if k.is_cuda or v.is_cuda:
             raise ShapeError("q, k and v must all be host tensors or all CUDA tensors")
         return _forward_from_host(q, k, v, shape, cfg, lse, workspace, heads_per_chunk)
     q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+    if morton:
+        from .errors import MissingGridError
+        from .reorder import device_permutation, permuted_forward
+        if grid_dims is None:
+            raise MissingGridError("morton=True needs grid_dims")
+        t, hh, w = grid_dims
+        if t * hh * w != T - t_t:
+            raise ShapeError(f"grid_dims product {t * hh * w} != T_v={T - t_t}")
+        out = permuted_forward(q, k, v, shape, cfg, device_permutation(grid_dims, q.device), lse, workspace)
+        if check_status:
+            nat.check(nat.lib().rsa_check_device_status(_ptr(workspace), _stream()))
+        return out
     if workspace is None:
         workspace = workspace_for(shape, q.device)
     out = torch.empty_like(q)

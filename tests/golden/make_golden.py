@@ -194,12 +194,30 @@ def large_goldens(rt) -> None:
     np.savez_compressed(HERE / "large_masks.npz", **out)
 
 
+MORTON_GRIDS = ((2, 4, 4), (3, 5, 7), (1, 60, 64), (29, 4, 6), (5, 16, 12))
+
+
+def morton_goldens(rt) -> None:
+    """rectattn.core.morton_permutation (core.py:276-291) on a few grids, and a
+    reorder_morton round trip of a cfg1-style problem (core.py:294-318)."""
+    out = {}
+    for g in MORTON_GRIDS:
+        out["perm_%d_%d_%d" % g] = rt.core.morton_permutation(g).astype(np.int32)
+    np.savez_compressed(HERE / "morton_perms.npz", **out)
+
+
 def main():
+    if "--morton-only" in sys.argv:
+        sys.path.insert(0, "/root/reference/pkg/src")
+        import rectattn as rt
+        morton_goldens(rt)
+        return
     with tempfile.TemporaryDirectory() as tmp:
         reference_fixtures(Path(tmp))
         import rectattn as rt
         tiny_goldens(rt)
         cfg1_goldens(rt)
+        morton_goldens(rt)
         if "--no-large" not in sys.argv:
             large_goldens(rt)
     (HERE / "README.md").write_text(
