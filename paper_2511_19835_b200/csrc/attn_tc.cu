@@ -655,8 +655,8 @@ __device__ __forceinline__ void mma_loop(const CUtensorMap& tm_k, const CUtensor
   }
 }
 
-template <int D, int BKV>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int D, int BKV, int WPQ, int EMU>
+__global__ void __launch_bounds__(128 + 128 * WPQ, 1)
 attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                           const TcParams P, int64_t n_tiles) {
   using C = Cfg<D, BKV, true, false>;
@@ -671,20 +671,20 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid
   uint64_t* p_full = s_full + C::NS;       // [NS]
   uint64_t* pv_done = p_full + C::NS;      // [1]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 1);
-  float* red_max = reinterpret_cast<float*>(bars + 32);   // [2][2][128] row maxima + [2][128] row sums
+  float* red_max = reinterpret_cast<float*>(bars + 32);   // [2][WPQ][128] row maxima + [WPQ][128] row sums
 
   const Geometry& g = P.g;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 
   if (threadIdx.x == 0) {
-    ptx::mbar_init(q_full, 256);
+    ptx::mbar_init(q_full, 128 * WPQ);
     for (int i = 0; i < C::NST; ++i) {
       ptx::mbar_init(kv_full + i, 1);
       ptx::mbar_init(kv_empty + i, 1);
     }
     for (int i = 0; i < C::NS; ++i) {
       ptx::mbar_init(s_full + i, 1);
-      ptx::mbar_init(p_full + i, 256);
+      ptx::mbar_init(p_full + i, 128 * WPQ);
     }
     ptx::mbar_init(pv_done, 1);
     ptx::fence_barrier_init();
@@ -701,11 +701,15 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid
     mma_loop<D, BKV>(tm_k, tm_v, P, n_tiles, kv_s, q_full, kv_full, kv_empty, s_full, p_full, pv_done, tmem, lane);
   } else if (warp >= 4) {
     // ===================== softmax + epilogue =====================
-    constexpr int HC = BKV / 2;     // score columns per thread
-    constexpr int HD = D / 2;       // output columns per thread
-    constexpr int QW = D / 4;       // 32-bit Q words per thread
+    // WPQ softmax warps per TMEM lane quadrant, each owning BKV / WPQ score
+    // columns and D / WPQ output columns of its quadrant's 32 rows
+    constexpr int HC = BKV / WPQ;   // score columns per thread
+    constexpr int HD = D / WPQ;     // output columns per thread
+    constexpr int QW = D / 2 / WPQ; // 32-bit Q words per thread
+    constexpr int NB = 32 * WPQ;    // threads of a quadrant's named barrier
+    static_assert(HC % 32 == 0 && HD % 32 == 0 && (QW == 16 || QW == 32), "column split");
     const int sw = warp - 4;
-    const int quad = sw & 3, half = sw >> 2;
+    const int quad = sw & 3, half = sw >> 2;   // half: column part 0..WPQ-1
     const int row = quad * 32 + lane;
     const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
     const int sub = row / (int)g.B;          // which member query block of the tile
@@ -718,7 +722,7 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid
       const int64_t grow = t.q_row0 + row;
       // permuted problem: gather the query row from its original position
       const int64_t srow = (P.perm && grow < g.Tv) ? P.perm[grow] : grow;
-      const uint4* src = reinterpret_cast<const uint4*>(P.q + (t.h * g.T + srow) * D + half * (D / 2));
+      const uint4* src = reinterpret_cast<const uint4*>(P.q + (t.h * g.T + srow) * D + half * (D / WPQ));
 #pragma unroll
       for (int i = 0; i < QW / 4; ++i) {
         const uint4 x = grow < g.T ? ptx::ld_stream(src + i, once) : make_uint4(0, 0, 0, 0);
@@ -776,9 +780,10 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid
 #pragma unroll
           for (int i = 0; i < 32; ++i) mx4[i & 3] = fmaxf(mx4[i & 3], __uint_as_float(sr[c][i]));
         float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
-        red_max[(gj & 1) * 256 + half * 128 + row] = mx;
-        asm volatile("bar.sync %0, 64;" ::"r"(1 + quad) : "memory");   // the quad's two warps only
-        mx = fmaxf(mx, red_max[(gj & 1) * 256 + (half ^ 1) * 128 + row]);
+        red_max[(gj & 1) * (WPQ * 128) + half * 128 + row] = mx;
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + quad), "r"(NB) : "memory");   // the quad's warps only
+#pragma unroll
+        for (int p2 = 0; p2 < WPQ; ++p2) mx = fmaxf(mx, red_max[(gj & 1) * (WPQ * 128) + p2 * 128 + row]);
         const float m_blk = mx * sl2;              // -inf if the row retains nothing here
         const float m_old = m_run;
         float alpha = 1.f;
@@ -798,7 +803,8 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid
           for (int i = 0; i < 16; ++i) {
             const float2 x = ptx::ffma2(make_float2(__uint_as_float(sr[c][2 * i]), __uint_as_float(sr[c][2 * i + 1])),
                                         sc2, nb2);
-            const float2 p = make_float2(ptx::ex2(x.x), ptx::ex2(x.y));
+            // EMU of every 8 pairs on the FMA pipe (polynomial), the rest on MUFU
+            const float2 p = (i & 7) < EMU ? ptx::ex2_poly2(x) : make_float2(ptx::ex2(x.x), ptx::ex2(x.y));
             sum2[i & 1] = ptx::fadd2(sum2[i & 1], p);
             pk[i] = ptx::pack_bf16(p.x, p.y);
           }
@@ -836,9 +842,11 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid
       }
 
       // ---- epilogue: O / l, rectification (rectify.py:66-89), bf16 store, LSE ----
-      red_max[512 + half * 128 + row] = l_part;
-      asm volatile("bar.sync %0, 64;" ::"r"(1 + quad) : "memory");   // the quad's two warps only
-      const float l_run = l_part + red_max[512 + (half ^ 1) * 128 + row];
+      red_max[2 * WPQ * 128 + half * 128 + row] = l_part;
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + quad), "r"(NB) : "memory");   // the quad's warps only
+      float l_run = 0.f;
+#pragma unroll
+      for (int p2 = 0; p2 < WPQ; ++p2) l_run += red_max[2 * WPQ * 128 + p2 * 128 + row];
       if (count > 0) {
         ptx::mbar_wait(pv_done, (uint32_t)((gs + count - 1) & 1));
         ptx::tc_fence_after();
@@ -1018,7 +1026,7 @@ bool make_tmap_3d(CUtensorMap* tm, const void* ptr, int64_t dim0, int64_t dim1, 
   return r == CUDA_SUCCESS;
 }
 
-template <int D, int BKV>
+template <int D, int BKV, int WPQ, int EMU = 0>
 cudaError_t launch_persistent(const Geometry& g, const void* q, const void* k, const void* v, void* out,
                               float* lse, const Workspace& ws, bool rectify, bool text, cudaStream_t st,
                               const int32_t* perm) {
@@ -1042,14 +1050,15 @@ cudaError_t launch_persistent(const Geometry& g, const void* q, const void* k, c
   P.text_part = ws.text_part;
   P.text_ml = reinterpret_cast<float2*>(ws.text_ml);
   P.scale_log2 = (float)(1.4426950408889634 / sqrt((double)g.d));
-  auto kern = attn_tc_persistent_kernel<D, BKV>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  auto kern = attn_tc_persistent_kernel<D, BKV, WPQ, EMU>;
+  const int smem = C::SMEM - 768 * 4 + 3 * WPQ * 128 * 4;   // row-max / row-sum exchange area
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t n_tiles = g.H * P.tiles_per_head;
-  kern<<<(unsigned)std::min<int64_t>(n_tiles, sms), kThreads, C::SMEM, st>>>(tk, tv, P, n_tiles);
+  kern<<<(unsigned)std::min<int64_t>(n_tiles, sms), 128 + 128 * WPQ, smem, st>>>(tk, tv, P, n_tiles);
   e = cudaGetLastError();
   if (e != cudaSuccess || P.text_tiles_per_head == 0) return e;
   text_combine_kernel<D><<<(unsigned)(g.H * P.text_tiles_per_head), 256, 0, st>>>(
@@ -1124,9 +1133,15 @@ cudaError_t launch_attn_tc(const Geometry& g, const void* q, const void* k, cons
   const int sel = (qtm ? 2 : 0) + (vt ? 1 : 0);
   // RSA_TC_PERSIST=0: one CTA per tile (attn_tc_kernel, with the diagnostic modes)
   static const int persist = [] { const char* e = getenv("RSA_TC_PERSIST"); return e ? atoi(e) : 1; }();
+  // RSA_TC_PEMU=n: n of every 8 ex2 pairs on the FMA pipe in the persistent kernel
+  static const int pemu = [] { const char* e = getenv("RSA_TC_PEMU"); return e ? atoi(e) : 0; }();
   if (persist && qtm && !vt && emu == 0) {
+    if (g.d == 128 && g.B == 128 && pemu == 1)
+      return launch_persistent<128, 128, 2, 1>(g, q, k, v, out, lse, ws, rectify, text, st, perm);
+    if (g.d == 128 && g.B == 128 && pemu == 2)
+      return launch_persistent<128, 128, 2, 2>(g, q, k, v, out, lse, ws, rectify, text, st, perm);
 #define RSA_TC_P(DD, BB) \
-  if (g.d == DD && g.B == BB) return launch_persistent<DD, BB>(g, q, k, v, out, lse, ws, rectify, text, st, perm);
+  if (g.d == DD && g.B == BB) return launch_persistent<DD, BB, 2>(g, q, k, v, out, lse, ws, rectify, text, st, perm);
     RSA_TC_P(128, 128)
     RSA_TC_P(128, 64)
     RSA_TC_P(64, 128)
