@@ -103,6 +103,7 @@ typedef struct {
   size_t v_t;         /* bf16 [d][T]   V transposed (tcgen05 path: K-major PV operand) */
   size_t text_part;   /* f32 [text tiles][chunks][128][d] split-K partial O of text queries */
   size_t text_ml;     /* f32 [text tiles][chunks][128][2] partial row max (log2) and row sum */
+  size_t a_applied;   /* [N][M]        a_pool where compensation is applied, else 0        */
   size_t status;      /* i32 [4]       device status flags (degenerate row, ...)     */
   size_t total;
 } rsa_workspace_layout;

@@ -45,7 +45,7 @@ class Grid(C.Structure):
 
 
 LAYOUT_FIELDS = ("q_pool", "q_def", "k_cat", "k_def", "v_pool", "scores", "a_pool", "mask_bits",
-                 "r", "r_eff", "comp", "kv_count", "kv_list", "tile_count", "tile_list", "v_t", "text_part", "text_ml",
+                 "r", "r_eff", "comp", "kv_count", "kv_list", "tile_count", "tile_list", "v_t", "text_part", "text_ml", "a_applied",
                  "status", "total")
 
 

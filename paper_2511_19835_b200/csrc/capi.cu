@@ -109,6 +109,7 @@ void layout_of(const rsa::Geometry& g, rsa_workspace_layout* L) {
   const size_t text_parts = g.dtype == RSA_BF16 ? H * (size_t)((g.Tt + 127) / 128) * rsa::text_chunks(g) * 128 : 0;
   L->text_part = take(text_parts * d * 4);
   L->text_ml = take(text_parts * 8);
+  L->a_applied = take(H * N * M * 8);
   L->total = off;
 }
 
@@ -136,6 +137,7 @@ rsa::Workspace bind(const rsa::Geometry& g, void* base) {
   w.v_t = reinterpret_cast<__nv_bfloat16*>(b + L.v_t);
   w.text_part = reinterpret_cast<float*>(b + L.text_part);
   w.text_ml = reinterpret_cast<float*>(b + L.text_ml);
+  w.a_applied = reinterpret_cast<double*>(b + L.a_applied);
   return w;
 }
 

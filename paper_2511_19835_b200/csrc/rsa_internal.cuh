@@ -30,6 +30,7 @@ struct Workspace {
   __nv_bfloat16* v_t;   // [H][d][T] transposed V (tcgen05 path)
   float* text_part;     // [H][text tiles][chunks][128][d] split-K text partial O (tcgen05 path)
   float* text_ml;       // [H][text tiles][chunks][128][2] partial row max (log2) and sum
+  double* a_applied;    // [H][N][M] a_pool where compensation is applied, else 0 (GEMM operand)
   int32_t* status;
 };
 

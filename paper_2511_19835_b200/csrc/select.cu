@@ -22,82 +22,13 @@
 // numpy's stable argsort of -a_pool.
 #include "rsa_internal.cuh"
 
+#include <cublas_v2.h>
+
 #include <cfloat>
 #include <cstdlib>
 
 namespace rsa {
 namespace {
-
-// ----------------------------------------------------------------------------
-// fp64 GEMM: C[h][r][c] = scale_div( sum_k A[h][r][k] * B'[h][k][c] )
-//   NT (scores):       A = q_pool [N][d], B = k_cat [n_cols][d]
-//   NN (compensation): A = a_pool masked by the applied bit [N][M], B = v_pool [M][d]
-// 64x64 tile, BK = 16, 256 threads x (4x4) outputs; k accumulated in order.
-// ----------------------------------------------------------------------------
-constexpr int GT = 64, GK = 16;
-
-template <bool NT>
-__global__ void __launch_bounds__(256)
-dgemm_kernel(const double* __restrict__ A, const double* __restrict__ Bm,
-             const uint8_t* __restrict__ abits, double* __restrict__ C,
-             int64_t rows, int64_t cols, int64_t K,
-             int64_t a_hstride, int64_t b_hstride, int64_t c_hstride, double divisor) {
-  __shared__ double As[GK][GT + 1];
-  __shared__ double Bs[GK][GT + 1];
-  const int64_t h = blockIdx.z;
-  const int64_t r0 = (int64_t)blockIdx.y * GT, c0 = (int64_t)blockIdx.x * GT;
-  const double* Ah = A + h * a_hstride;
-  const double* Bh = Bm + h * b_hstride;
-  const uint8_t* bits = abits ? abits + h * a_hstride : nullptr;
-  const int tid = threadIdx.x;
-  const int tr = tid / 16, tc = tid % 16;
-  double acc[4][4] = {};
-  for (int64_t k0 = 0; k0 < K; k0 += GK) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int e = tid + i * 256;       // 0..1023
-      const int rr = e / GK, kk = e % GK;
-      const int64_t gr = r0 + rr, gk = k0 + kk;
-      double a = 0.0;
-      if (gr < rows && gk < K) {
-        a = Ah[gr * K + gk];
-        if (bits && !(bits[gr * K + gk] & BIT_APPLIED)) a = 0.0;
-      }
-      As[kk][rr] = a;
-      double b = 0.0;
-      if (NT) {
-        const int64_t gc = c0 + rr;
-        if (gc < cols && gk < K) b = Bh[gc * K + gk];
-        Bs[kk][rr] = b;
-      } else {
-        const int cc = e % GT, kb = e / GT;
-        const int64_t gc = c0 + cc, gkb = k0 + kb;
-        if (gc < cols && gkb < K) b = Bh[gkb * cols + gc];
-        Bs[kb][cc] = b;
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < GK; ++kk) {
-      double a[4], b[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) { a[i] = As[kk][tr + 16 * i]; b[i] = Bs[kk][tc + 16 * i]; }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
-    }
-    __syncthreads();
-  }
-  double* Ch = C + h * c_hstride;
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int64_t gr = r0 + tr + 16 * i, gc = c0 + tc + 16 * j;
-      if (gr < rows && gc < cols) Ch[gr * cols + gc] = divisor == 1.0 ? acc[i][j] : acc[i][j] / divisor;
-    }
-}
 
 // ----------------------------------------------------------------------------
 // block-wide deterministic reductions (fixed tree order)
@@ -163,6 +94,7 @@ struct SelectParams {
   int force_text;
   int variant;
   double inv_sqrt_d;
+  double sqrt_d;
   int p2;  // power of two >= M for the sort
   int use_sort;  // 1: top-K from one full bitonic sort of the row (no radix select)
 };
@@ -210,7 +142,11 @@ __global__ void __launch_bounds__(RT) select_rows_kernel(SelectParams P) {
   __shared__ unsigned hist[256];
   __shared__ int sh_digit, sh_rem;
 
-  const double* srow = ws.scores + (h * N + n) * n_cols;
+  // the scores GEMM (cuBLAS) leaves q_pool . k_cat^T; divide by sqrt(d) here
+  // (ipar.py:41, masks.py:127 divide, they do not multiply by 1/sqrt(d))
+  double* srow = ws.scores + (h * N + n) * n_cols;
+  for (int64_t j = threadIdx.x; j < n_cols; j += RT) srow[j] = srow[j] / P.sqrt_d;
+  __syncthreads();
 
   // ---- IPAR: softmax over the mixed row (core.py:204-208) ----
   double mx = -DBL_MAX;
@@ -444,7 +380,11 @@ __global__ void __launch_bounds__(RT) select_rows_kernel(SelectParams P) {
   }
   __syncthreads();
   uint8_t* bits_out = ws.mask_bits + (h * N + n) * M;
-  for (int64_t m = threadIdx.x; m < M; m += RT) bits_out[m] = bits[m];
+  double* applied_out = ws.a_applied + (h * N + n) * M;   // operand of the compensation GEMM
+  for (int64_t m = threadIdx.x; m < M; m += RT) {
+    bits_out[m] = bits[m];
+    applied_out[m] = (bits[m] & BIT_APPLIED) ? ap[m] : 0.0;
+  }
   if (threadIdx.x == 0) {
     ws.r[h * N + n] = R;
     const bool rect = P.variant == RSA_VARIANT_SPARSE_RECTIFIED ||
@@ -521,17 +461,31 @@ __global__ void tile_lists_kernel(Workspace ws, Geometry g) {
   if (lane == 0) ws.tile_count[h * tiles_per_head + t] = count;
 }
 
+// one cuBLAS handle per host thread and device (the fp64 GEMMs of K2)
+cublasHandle_t cublas_handle() {
+  static thread_local cublasHandle_t handles[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  if (!handles[dev] && cublasCreate(&handles[dev]) != CUBLAS_STATUS_SUCCESS) handles[dev] = nullptr;
+  return handles[dev];
+}
+
 }  // namespace
 
 cudaError_t launch_select(const Geometry& g, const rsa_config& cfg, int64_t k_floor,
                           const Workspace& ws, cudaStream_t st, int* launches) {
   const double sqrt_d = sqrt((double)g.d);
-  // scores = (q_pool @ k_cat^T) / sqrt(d)   (ipar.py:41, masks.py:127)
+  // scores = q_pool @ k_cat^T (select_rows divides by sqrt(d)): a plain
+  // strided-batched fp64 GEMM, row-major [N][n_cols] = column-major n_cols x N
+  cublasHandle_t hb = cublas_handle();
+  if (!hb) return cudaErrorInitializationError;
+  if (cublasSetStream(hb, st) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
   {
-    dim3 grid((unsigned)((g.n_cols + GT - 1) / GT), (unsigned)((g.N + GT - 1) / GT), (unsigned)g.H);
-    dgemm_kernel<true><<<grid, 256, 0, st>>>(ws.q_pool, ws.k_cat, nullptr, ws.scores, g.N,
-                                             g.n_cols, g.d, g.N * g.d, g.n_cols * g.d,
-                                             g.N * g.n_cols, sqrt_d);
+    const double one = 1.0, zero = 0.0;
+    if (cublasDgemmStridedBatched(hb, CUBLAS_OP_T, CUBLAS_OP_N, (int)g.n_cols, (int)g.N, (int)g.d, &one,
+                                  ws.k_cat, (int)g.d, g.n_cols * g.d, ws.q_pool, (int)g.d, g.N * g.d, &zero,
+                                  ws.scores, (int)g.n_cols, g.N * g.n_cols, (int)g.H) != CUBLAS_STATUS_SUCCESS)
+      return cudaErrorUnknown;
     ++*launches;
   }
   SelectParams P;
@@ -543,6 +497,7 @@ cudaError_t launch_select(const Geometry& g, const rsa_config& cfg, int64_t k_fl
   P.force_text = cfg.force_text_blocks;
   P.variant = cfg.variant;
   P.inv_sqrt_d = 1.0 / sqrt_d;
+  P.sqrt_d = sqrt_d;
   int p2 = 1;
   while (p2 < g.M) p2 <<= 1;
   P.p2 = p2;
@@ -554,11 +509,14 @@ cudaError_t launch_select(const Geometry& g, const rsa_config& cfg, int64_t k_fl
   }
   select_rows_kernel<<<dim3((unsigned)g.N, (unsigned)g.H), RT, smem, st>>>(P);
   ++*launches;
-  // compensation rows: (a_pool masked to applied) @ v_pool   (rectify.py:84-87)
+  // compensation rows: (a_pool masked to applied) @ v_pool   (rectify.py:84-87);
+  // select_rows wrote the masked operand.  Row-major [N][d] = col-major d x N
   {
-    dim3 grid((unsigned)((g.d + GT - 1) / GT), (unsigned)((g.N + GT - 1) / GT), (unsigned)g.H);
-    dgemm_kernel<false><<<grid, 256, 0, st>>>(ws.a_pool, ws.v_pool, ws.mask_bits, ws.comp, g.N,
-                                              g.d, g.M, g.N * g.M, g.M * g.d, g.N * g.d, 1.0);
+    const double one = 1.0, zero = 0.0;
+    if (cublasDgemmStridedBatched(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)g.d, (int)g.N, (int)g.M, &one,
+                                  ws.v_pool, (int)g.d, g.M * g.d, ws.a_applied, (int)g.M, g.N * g.M, &zero,
+                                  ws.comp, (int)g.d, g.N * g.d, (int)g.H) != CUBLAS_STATUS_SUCCESS)
+      return cudaErrorUnknown;
     ++*launches;
   }
   return cudaGetLastError();
