@@ -198,6 +198,20 @@ rsa_status rsa_forward_permuted(const rsa_shape* shape, const rsa_config* cfg, c
                                 const void* k, const void* v, const int32_t* perm, void* perm_buf,
                                 void* out, float* lse, void* workspace, void* stream);
 
+/* Validation diagnostics (quadratic; fp64 like the reference), after
+ * rsa_pool + rsa_select on `workspace`.  Outputs (device, fp64):
+ *   gain, error, exact_gain, exact_error  [heads][N][M]  -- gain_error(...,
+ *       with_exact=True), masks.py:189-219 (the relaxed pair is what K2 gates on)
+ *   s_sum, s_sum_pool                      [heads][t_video] -- the true and
+ *       pooled softmax denominators of denominator_equivalence_report,
+ *       metrics.py:90-113
+ * gapr_condition_agreement (metrics.py:116-124) and the satisfied fraction
+ * follow from them.  `scratch`: rsa_diagnostics_scratch_size() bytes. */
+size_t rsa_diagnostics_scratch_size(const rsa_shape* shape);
+rsa_status rsa_diagnostics(const rsa_shape* shape, const void* q, const void* k, void* workspace,
+                           double* gain, double* error, double* exact_gain, double* exact_error,
+                           double* s_sum, double* s_sum_pool, void* scratch, void* stream);
+
 /* Synchronises `stream` and converts device-side status flags (e.g. a
  * reallocation denominator <= 0, ipar.py:62-64) into an rsa_status. */
 rsa_status rsa_check_device_status(void* workspace, void* stream);

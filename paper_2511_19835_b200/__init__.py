@@ -10,6 +10,7 @@ rectification epilogue).  There is no CPU fallback.
 from .core import (VARIANTS, AttentionOutput, AttentionProblem, BlockGrid, CompensationMask,
                    ImplicitAttention, PipelineAccounting, PipelineResult, PooledSet,
                    RectificationFactors, SparseMask, SparsityConfig, check_result_invariants,
+                   DenominatorReport, GainError,
                    partition, sparsity_and_flops)
 from .errors import (BlockSizeError, ConfigError, DegenerateRowError, EmptyRowError, IoError,
                      MissingGridError, NativeError, RectAttnError, SchemaError, ShapeError,
@@ -20,6 +21,7 @@ __version__ = "0.1.0"
 _LAZY = {"rectified_attention_pipeline", "block_sparse_attention", "text_full_attention",
          "rectified_sparse_attention"}
 _REORDER = {"morton_permutation", "reorder_morton", "inverse_permutation"}
+_DIAG = {"gain_error", "gapr_condition_agreement", "denominator_equivalence_report"}
 
 
 def __getattr__(name):
@@ -30,4 +32,7 @@ def __getattr__(name):
     if name in _REORDER:
         from . import reorder
         return getattr(reorder, name)
+    if name in _DIAG:
+        from . import diagnostics
+        return getattr(diagnostics, name)
     raise AttributeError(name)

@@ -244,6 +244,28 @@ class SparseMask:
 
 
 @dataclass(frozen=True, eq=False)
+class GainError:
+    """Relaxed-form gain and pooling error per block, with the optional exact
+    softmax-form values kept for validation (masks.py:58-66)."""
+
+    gain: object
+    error: object
+    exact_gain: object | None = None
+    exact_error: object | None = None
+
+
+@dataclass(frozen=True, eq=False)
+class DenominatorReport:
+    """Per-video-token softmax denominators, true vs pooled, and the fraction
+    within a relative threshold of each other (metrics.py:35-43)."""
+
+    s_sum: object
+    s_sum_pool: object
+    satisfied_fraction: float
+    tau: float
+
+
+@dataclass(frozen=True, eq=False)
 class CompensationMask:
     """masks.py:69-73: consumed as ``~sparse.mask & mask``."""
 

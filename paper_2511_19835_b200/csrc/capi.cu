@@ -435,6 +435,28 @@ rsa_status rsa_forward_permuted(const rsa_shape* shape, const rsa_config* cfg, c
   return run_attention(shape, g, ws, q, kp, vp, out, lse, rectifies(cfg->variant), true, st, perm);
 }
 
+size_t rsa_diagnostics_scratch_size(const rsa_shape* shape) {
+  rsa::Geometry g;
+  if (make_geometry(shape, &g) != RSA_OK) return 0;
+  return rsa::diag_scratch_size(g);
+}
+
+rsa_status rsa_diagnostics(const rsa_shape* shape, const void* q, const void* k, void* workspace, double* gain,
+                           double* error, double* exact_gain, double* exact_error, double* s_sum,
+                           double* s_sum_pool, void* scratch, void* stream) {
+  g_launches = 0;
+  rsa::Geometry g;
+  rsa_status s = make_geometry(shape, &g);
+  if (s != RSA_OK) return s;
+  if (!q || !k || !workspace || !gain || !error || !exact_gain || !exact_error || !s_sum || !s_sum_pool || !scratch)
+    return fail(RSA_ERR_SHAPE, "null pointer");
+  rsa::Workspace ws = bind(g, workspace);
+  cudaError_t e = rsa::launch_diagnostics(g, q, k, ws, gain, error, exact_gain, exact_error, s_sum, s_sum_pool,
+                                          scratch, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "diagnostics");
+  return RSA_OK;
+}
+
 rsa_status rsa_check_device_status(void* workspace, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int32_t flags[4] = {0, 0, 0, 0};

@@ -89,6 +89,10 @@ cudaError_t launch_attn_simt(const Geometry& g, const void* q, const void* k, co
                              bool text, cudaStream_t st, int* launches);
 bool tc_supported(const Geometry& g);
 void morton_permutation_host(int64_t t, int64_t h, int64_t w, int32_t* perm);
+size_t diag_scratch_size(const Geometry& g);
+cudaError_t launch_diagnostics(const Geometry& g, const void* q, const void* k, const Workspace& ws,
+                               double* gain, double* error, double* exact_gain, double* exact_error,
+                               double* s_sum, double* s_sum_pool, void* scratch, cudaStream_t st);
 cudaError_t launch_permute_rows(const Geometry& g, const int32_t* perm, const void* src, void* dst,
                                 bool inverse, cudaStream_t st);
 cudaError_t launch_attn_tc(const Geometry& g, const void* q, const void* k, const void* v,

@@ -145,12 +145,14 @@ __global__ void __launch_bounds__(RT) select_rows_kernel(SelectParams P) {
   // the scores GEMM (cuBLAS) leaves q_pool . k_cat^T; divide by sqrt(d) here
   // (ipar.py:41, masks.py:127 divide, they do not multiply by 1/sqrt(d))
   double* srow = ws.scores + (h * N + n) * n_cols;
-  for (int64_t j = threadIdx.x; j < n_cols; j += RT) srow[j] = srow[j] / P.sqrt_d;
-  __syncthreads();
 
   // ---- IPAR: softmax over the mixed row (core.py:204-208) ----
   double mx = -DBL_MAX;
-  for (int64_t j = threadIdx.x; j < n_mix; j += RT) { const double s = srow[j]; sa[j] = s; mx = fmax(mx, s); }
+  for (int64_t j = threadIdx.x; j < n_cols; j += RT) {
+    const double s = srow[j] / P.sqrt_d;
+    srow[j] = s;
+    if (j < n_mix) { sa[j] = s; mx = fmax(mx, s); }
+  }
   mx = block_max(mx, red);
   double part = 0.0;
   for (int64_t j = threadIdx.x; j < n_mix; j += RT) { const double e = exp(sa[j] - mx); sa[j] = e; part += e; }

@@ -206,7 +206,40 @@ def morton_goldens(rt) -> None:
     np.savez_compressed(HERE / "morton_perms.npz", **out)
 
 
+DIAG_CASES = ((3, 96, 20, 16, 8), (5, 128, 0, 8, 16), (7, 64, 37, 32, 16))
+
+
+def diag_goldens(rt) -> None:
+    """Reference validation diagnostics on small problems (random_problem
+    inputs, regenerated from the seed by the tests): gain_error(with_exact=True)
+    (masks.py:189-219), denominator_equivalence_report (metrics.py:90-113),
+    gapr_condition_agreement (metrics.py:116-124)."""
+    from oracle import rsa_oracle as O
+    from rectattn.masks import gain_error
+    from rectattn.metrics import denominator_equivalence_report, gapr_condition_agreement
+    out = {}
+    for seed, t_v, t_t, d, b in DIAG_CASES:
+        qv, qt, k, v = O.random_problem(seed, t_v=t_v, t_t=t_t, d=d)
+        prob = rt.AttentionProblem(q_video=qv, q_text=qt, k=k, v=v, d=d, block=b)
+        grid = rt.partition(prob)
+        pooled = rt.pool_problem(prob, grid)
+        ge = gain_error(prob, pooled, grid, with_exact=True)
+        rep = denominator_equivalence_report(prob, pooled, grid)
+        tag = f"s{seed}"
+        out[f"{tag}_gain"], out[f"{tag}_error"] = ge.gain, ge.error
+        out[f"{tag}_exact_gain"], out[f"{tag}_exact_error"] = ge.exact_gain, ge.exact_error
+        out[f"{tag}_s_sum"], out[f"{tag}_s_sum_pool"] = rep.s_sum, rep.s_sum_pool
+        out[f"{tag}_satisfied"] = np.array(rep.satisfied_fraction)
+        out[f"{tag}_agreement"] = np.array(gapr_condition_agreement(prob, pooled, grid))
+    np.savez_compressed(HERE / "diagnostics.npz", **out)
+
+
 def main():
+    if "--diag-only" in sys.argv:
+        sys.path.insert(0, "/root/reference/pkg/src")
+        import rectattn as rt
+        diag_goldens(rt)
+        return
     if "--morton-only" in sys.argv:
         sys.path.insert(0, "/root/reference/pkg/src")
         import rectattn as rt
@@ -218,6 +251,7 @@ def main():
         tiny_goldens(rt)
         cfg1_goldens(rt)
         morton_goldens(rt)
+        diag_goldens(rt)
         if "--no-large" not in sys.argv:
             large_goldens(rt)
     (HERE / "README.md").write_text(
