@@ -234,7 +234,29 @@ def diag_goldens(rt) -> None:
     np.savez_compressed(HERE / "diagnostics.npz", **out)
 
 
+def rsat_goldens(rt) -> None:
+    """Bytes of RSAT files written by the reference writer (rsat.py:17-35)."""
+    import tempfile as tf
+    from rectattn.rsat import write_rsat
+    rng = np.random.default_rng(5)
+    arrays = {"f32_2d": rng.standard_normal((7, 5)).astype(np.float32),
+              "f64_3d": rng.standard_normal((2, 3, 4)), "f32_1d": np.arange(6, dtype=np.float32)}
+    out = {}
+    with tf.TemporaryDirectory() as tmp:
+        for name, a in arrays.items():
+            p = Path(tmp) / f"{name}.rsat"
+            write_rsat(p, a)
+            out[name] = a
+            out[name + "_bytes"] = np.frombuffer(p.read_bytes(), dtype=np.uint8)
+    np.savez_compressed(HERE / "rsat_files.npz", **out)
+
+
 def main():
+    if "--rsat-only" in sys.argv:
+        sys.path.insert(0, "/root/reference/pkg/src")
+        import rectattn as rt
+        rsat_goldens(rt)
+        return
     if "--diag-only" in sys.argv:
         sys.path.insert(0, "/root/reference/pkg/src")
         import rectattn as rt
@@ -252,6 +274,7 @@ def main():
         cfg1_goldens(rt)
         morton_goldens(rt)
         diag_goldens(rt)
+        rsat_goldens(rt)
         if "--no-large" not in sys.argv:
             large_goldens(rt)
     (HERE / "README.md").write_text(
