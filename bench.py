@@ -198,8 +198,14 @@ def cpu_reference_sample(cfg, f, variant, sample_blocks, seed=42):
     # single-threaded BLAS inside the oracle's per-query-block thread pool (all
     # host cores): numpy may already have started multi-threaded OpenBLAS when
     # torch was imported, which oversubscribes the cores 16x
+    # two heads (seeds 42, 43; extrapolate from >= 2 heads)
     with threadpool_limits(limits=1, user_api="blas"):
-        return _cpu_reference_sample(np, O, cfg, f, variant, sample_blocks, seed)
+        runs = [_cpu_reference_sample(np, O, cfg, f, variant, sample_blocks, seed + i) for i in range(2)]
+    per_head = sum(r["per_head_s"] for r in runs) / len(runs)
+    return {"ms_per_call": per_head * cfg["heads"] * 1e3, "sample_s": sum(r["sample_s"] for r in runs),
+            "per_head_s": per_head, "cores": runs[0]["cores"],
+            "sample": runs[0]["sample"].replace(f"1 head (seed {seed}) of", f"2 heads (seeds {seed}, {seed + 1}; "
+                                                                           f"mean per head) of")}
 
 
 def _cpu_reference_sample(np, O, cfg, f, variant, sample_blocks, seed):
