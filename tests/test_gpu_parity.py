@@ -256,7 +256,7 @@ def test_errors_map_to_reference_classes():
 # ---------------------------------------------------------------- tcgen05 kernel
 
 @pytest.mark.parametrize("d,block", [(64, 64), (64, 128), (128, 64), (128, 128)])
-@pytest.mark.parametrize("t_t", [0, 200])
+@pytest.mark.parametrize("t_t", [0, 1, 129, 200])
 def test_tcgen05_kernel_matches_oracle_and_simt(d, block, t_t):
     """The tensor-core K3 against the fp32 oracle pipeline and the CUDA-core
     K3 on bf16-valued inputs: ragged text tile and ragged last kv block
@@ -344,3 +344,24 @@ def test_forward_from_host_tensors_matches_device():
                                              heads_per_chunk=chunk)
         assert not got.is_cuda
         assert torch.equal(got, want), (pinned, chunk)
+
+
+def test_tcgen05_persistent_many_tiles_per_cta():
+    """More 128-row tiles than SMs (each persistent CTA walks several tiles of
+    several heads, text chunks and video tiles mixed): tensor-core output and
+    LSE against the CUDA-core kernel, and bitwise repeatable."""
+    heads, block, d, n_q, t_t = 5, 64, 64, 150, 77
+    t_v = block * n_q
+    g = torch.Generator().manual_seed(12)
+    q, k, v = (torch.randn(heads, t_v + t_t, d, generator=g).to(torch.bfloat16).cuda() for _ in range(3))
+    outs = {}
+    for kern in ("tcgen05", "simt", "tcgen05"):
+        lse = torch.empty(heads, t_v + t_t, dtype=torch.float32, device="cuda")
+        o = rsa.rectified_sparse_attention(q, k, v, num_text_tokens=t_t, block=block, top_k_fraction=0.15,
+                                           kernel=kern, lse=lse, check_status=True)
+        if kern in outs:
+            assert torch.equal(o, outs[kern][0]) and torch.equal(lse, outs[kern][1])
+        outs[kern] = (o, lse)
+    diff = (outs["tcgen05"][0].float() - outs["simt"][0].float()).abs().max().item()
+    assert diff <= 1e-2, diff
+    assert (outs["tcgen05"][1] - outs["simt"][1]).abs().max().item() <= 1e-2
