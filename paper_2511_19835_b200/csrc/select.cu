@@ -487,8 +487,7 @@ cudaError_t launch_select(const Geometry& g, const rsa_config& cfg, int64_t k_fl
     if (cublasDgemmStridedBatched(hb, CUBLAS_OP_T, CUBLAS_OP_N, (int)g.n_cols, (int)g.N, (int)g.d, &one,
                                   ws.k_cat, (int)g.d, g.n_cols * g.d, ws.q_pool, (int)g.d, g.N * g.d, &zero,
                                   ws.scores, (int)g.n_cols, g.N * g.n_cols, (int)g.H) != CUBLAS_STATUS_SUCCESS)
-      return cudaErrorUnknown;
-    ++*launches;
+      return cudaErrorUnknown;   // library kernel: not counted in *launches (ours only)
   }
   SelectParams P;
   P.g = g;
@@ -518,8 +517,7 @@ cudaError_t launch_select(const Geometry& g, const rsa_config& cfg, int64_t k_fl
     if (cublasDgemmStridedBatched(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)g.d, (int)g.N, (int)g.M, &one,
                                   ws.v_pool, (int)g.d, g.M * g.d, ws.a_applied, (int)g.M, g.N * g.M, &zero,
                                   ws.comp, (int)g.d, g.N * g.d, (int)g.H) != CUBLAS_STATUS_SUCCESS)
-      return cudaErrorUnknown;
-    ++*launches;
+      return cudaErrorUnknown;   // library kernel: not counted in *launches (ours only)
   }
   return cudaGetLastError();
 }
