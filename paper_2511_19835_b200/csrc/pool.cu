@@ -282,7 +282,7 @@ __device__ __forceinline__ PoolItem pool_item(const Geometry& g, int64_t i) {
 }
 
 template <int D, int STAGES>
-__global__ void __launch_bounds__(kBulkThreads, 2)
+__global__ void __launch_bounds__(kBulkThreads, 3)
 pool_bulk_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k,
                  const __nv_bfloat16* __restrict__ v, Workspace ws, Geometry g, int64_t n_items,
                  const int32_t* __restrict__ perm, __nv_bfloat16* kp, __nv_bfloat16* vp) {
@@ -464,7 +464,7 @@ pool_bulk_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
 template <int D>
 cudaError_t launch_bulk(const Geometry& g, const void* q, const void* k, const void* v, const Workspace& ws,
                         cudaStream_t st, const int32_t* perm, void* kp, void* vp) {
-  constexpr int STAGES = 3;
+  constexpr int STAGES = 2;
   constexpr int RP = kBulkThreads / (D / 2);
   const size_t smem = (size_t)STAGES * g.B * D * 2 + STAGES * 8 + 2 * RP * D * 8 + 64;
   auto kern = pool_bulk_kernel<D, STAGES>;
@@ -474,7 +474,7 @@ cudaError_t launch_bulk(const Geometry& g, const void* q, const void* k, const v
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t n_items = g.H * (g.N + 2 * g.M);
-  const int64_t grid = std::min<int64_t>(n_items, (int64_t)sms * 2);
+  const int64_t grid = std::min<int64_t>(n_items, (int64_t)sms * 3);
   kern<<<(unsigned)grid, kBulkThreads, smem, st>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
                                                    (const __nv_bfloat16*)v, ws, g, n_items, perm,
                                                    (__nv_bfloat16*)kp, (__nv_bfloat16*)vp);
@@ -505,9 +505,9 @@ cudaError_t launch_pool(const Geometry& g, const void* q, const void* k, const v
   switch (g.dtype) {
     case RSA_BF16: {
       // bulk-copy streaming path when a block is one 16-byte-aligned range
-      // that fits three ring stages per CTA, two CTAs per SM
+      // that fits two ring stages per CTA, three CTAs per SM
       const bool aligned = ((uintptr_t)q % 16 == 0) && ((uintptr_t)k % 16 == 0) && ((uintptr_t)v % 16 == 0);
-      const bool fits = g.B * g.d * 2 * 3 <= 96 * 1024;
+      const bool fits = g.B * g.d * 2 * 2 <= 64 * 1024;
       if (aligned && fits && g.d == 128) return launch_bulk<128>(g, q, k, v, ws, st, perm, kp, vp);
       if (aligned && fits && g.d == 64) return launch_bulk<64>(g, q, k, v, ws, st, perm, kp, vp);
       if (perm) return cudaErrorNotSupported;
