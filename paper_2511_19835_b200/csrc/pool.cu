@@ -309,27 +309,42 @@ pool_bulk_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  // Stage item i into ring slot s (warp 0).  With a token permutation `perm`
-  // (video row r of the permuted problem = original row perm[r]) a video
-  // block is gathered row by row, 4 rows per lane; text blocks and the
-  // identity order are one contiguous copy.
+  // Stage item i into ring slot s (thread 0): one contiguous bulk copy.
   auto fetch = [&](int64_t i, int s) {
     const PoolItem it = pool_item(g, i);
     uint32_t bytes;
     const void* src = src_of(it, bytes);
     uint8_t* dst = ring + s * stage_bytes;
-    if (perm && it.blk < g.N) {
-      if (t == 0) bar_expect_tx(full + s, bytes);
-      __syncwarp();
-      const __nv_bfloat16* base = it.seg == 0 ? q : it.seg == 1 ? k : v;
-      for (int r = t; r < g.B; r += 32)
-        bulk_g2s(dst + r * D * 2, base + (it.h * g.T + perm[it.blk * g.B + r]) * D, D * 2, full + s);
-    } else if (t == 0) {
+    if (t == 0) {
       bar_expect_tx(full + s, bytes);
       bulk_g2s(dst, src, bytes, full + s);
     }
   };
-  if (t < 32) {
+  // Permuted problem: every thread gathers 16-byte pieces of the block's rows
+  // (LDGSTS, cp.async groups) -- 128 row-sized bulk copies per block keep the
+  // TMA engine busy issuing instead of moving bytes.
+  constexpr int CPR = D * 2 / 16;   // 16-byte pieces per row
+  auto fetch_rows = [&](int64_t i, int s) {
+    const PoolItem it = pool_item(g, i);
+    const int64_t len = (it.blk < g.N) ? g.B : (it.blk == g.M - 1 ? g.last_len : g.B);
+    const __nv_bfloat16* base = (it.seg == 0 ? q : it.seg == 1 ? k : v) + it.h * g.T * D;
+    uint8_t* dst = ring + s * stage_bytes;
+    for (int64_t c = t; c < len * CPR; c += kBulkThreads) {
+      const int64_t r = c / CPR, cc = c % CPR;
+      const int64_t row = it.blk < g.N ? perm[it.blk * g.B + r] : it.blk * g.B + r;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(dst + r * D * 2 + cc * 16)),
+                   "l"(base + row * D + cc * 8)
+                   : "memory");
+    }
+  };
+  if (perm) {
+    for (int s = 0; s < STAGES; ++s) {
+      const int64_t i = blockIdx.x + (int64_t)s * gridDim.x;
+      if (i < n_items) fetch_rows(i, s);
+      asm volatile("cp.async.commit_group;" ::: "memory");   // one group per stage, even if empty
+    }
+  } else if (t < 32) {
     for (int s = 0; s < STAGES; ++s) {
       const int64_t i = blockIdx.x + (int64_t)s * gridDim.x;
       if (i >= n_items) break;
@@ -341,9 +356,16 @@ pool_bulk_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
     const int s = (int)(kk % STAGES);
     const PoolItem it = pool_item(g, i);
     const int64_t len = (it.blk < g.N) ? g.B : (it.blk == g.M - 1 ? g.last_len : g.B);
-    bar_wait(full + s, (uint32_t)((kk / STAGES) & 1));
+    if (perm) {
+      // this item's group (committed STAGES groups ago) has landed, all threads' pieces
+      asm volatile("cp.async.wait_group %0;" ::"n"(STAGES - 1) : "memory");
+      __syncthreads();
+    } else {
+      bar_wait(full + s, (uint32_t)((kk / STAGES) & 1));
+    }
     const uint32_t* blk = reinterpret_cast<const uint32_t*>(ring + s * stage_bytes);
     if (kp && it.seg > 0 && t == 0) {
+      if (perm) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> bulk read
       // the permuted K / V block, contiguous, for K3's TMA (shared -> global bulk copy)
       __nv_bfloat16* dstp = (it.seg == 1 ? kp : vp) + (it.h * g.T + it.blk * g.B) * D;
       asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n\t"
@@ -420,7 +442,13 @@ pool_bulk_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
     }
     // stage s is free (its permuted copy, if any, has been read out): refill
     // it with this CTA's item STAGES ahead
-    if (t < 32) {
+    if (perm) {
+      if (t == 0 && kp) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      __syncthreads();
+      const int64_t nx = i + (int64_t)STAGES * gridDim.x;
+      if (nx < n_items) fetch_rows(nx, s);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    } else if (t < 32) {
       if (t == 0 && kp) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       __syncwarp();
       const int64_t nx = i + (int64_t)STAGES * gridDim.x;
