@@ -744,7 +744,12 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid
       t = decode_tile(P, bid);
       store_q(t);
     }
-    for (; bid < n_tiles; bid += gridDim.x) {
+    // RSA_TC_STAMPS=3: per-tile clock64 stamps of CTA trace_cta (profiling):
+    // [tile][0] first S ready, [1] last P done, [2] next Q stored, [3] epilogue done
+    long long* tt = (P.stamps == 3 && P.lse && blockIdx.x == (unsigned)P.trace_cta && sw == 0 && lane == 0)
+                        ? reinterpret_cast<long long*>(P.lse) : nullptr;
+    int tix = 0;
+    for (; bid < n_tiles; bid += gridDim.x, ++tix) {
       const int64_t count = t.count;
       float m_run = -INFINITY, l_part = 0.f;
       for (int64_t j = 0; j < count; ++j) {
@@ -761,6 +766,7 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid
         }
         const int len = (m == g.M - 1 && g.n_text > 0) ? (int)g.last_len : (int)g.B;
         ptx::mbar_wait(s_full + (gj % C::NS), (uint32_t)((gj / C::NS) & 1));
+        if (tt && j == 0 && tix < 256) tt[tix * 4 + 0] = clock64();
         ptx::tc_fence_after();
         const uint32_t s_addr = lane_base + (uint32_t)((gj % C::NS) * BKV);
         uint32_t sr[HC / 32][32];
@@ -834,12 +840,14 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid
       }
       // every S of this tile has been read: Q's TMEM columns are free, so the
       // next tile's Q goes in now and its S_0, S_1 overlap this epilogue
+      if (tt && tix < 256) tt[tix * 4 + 1] = clock64();
       const TileDesc cur = t;
       const int64_t nb = bid + gridDim.x;
       if (nb < n_tiles) {
         t = decode_tile(P, nb);
         store_q(t);
       }
+      if (tt && tix < 256) tt[tix * 4 + 2] = clock64();
 
       // ---- epilogue: O / l, rectification (rectify.py:66-89), bf16 store, LSE ----
       red_max[2 * WPQ * 128 + half * 128 + row] = l_part;
@@ -907,11 +915,12 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid
             }
           }
         }
-        if (valid && half == 0 && P.lse)
+        if (valid && half == 0 && P.lse && !P.stamps)
           P.lse[cur.h * g.T + orig] = l_run > 0.f ? (log2f(l_run) + m_run) * 0.69314718055994531f : -INFINITY;
       }
       // O is read: the next tile's PV_0 (after its P_0 below) may overwrite it
       ptx::tc_fence_before();
+      if (tt && tix < 256) tt[tix * 4 + 3] = clock64();
       gs += count;
     }
   }
@@ -1050,6 +1059,10 @@ cudaError_t launch_persistent(const Geometry& g, const void* q, const void* k, c
   P.text_part = ws.text_part;
   P.text_ml = reinterpret_cast<float2*>(ws.text_ml);
   P.scale_log2 = (float)(1.4426950408889634 / sqrt((double)g.d));
+  const char* sp = getenv("RSA_TC_STAMPS");
+  P.stamps = sp ? atoi(sp) : 0;
+  const char* tc_cta = getenv("RSA_TC_TRACE_CTA");
+  P.trace_cta = tc_cta ? atoi(tc_cta) : 0;
   auto kern = attn_tc_persistent_kernel<D, BKV, WPQ, EMU>;
   const int smem = C::SMEM - 768 * 4 + 3 * WPQ * 128 * 4;   // row-max / row-sum exchange area
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
