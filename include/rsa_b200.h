@@ -212,6 +212,14 @@ rsa_status rsa_diagnostics(const rsa_shape* shape, const void* q, const void* k,
                            double* gain, double* error, double* exact_gain, double* exact_error,
                            double* s_sum, double* s_sum_pool, void* scratch, void* stream);
 
+/* The reference's ground truth, full_attention_oracle (core.py:211-225):
+ * dense fp64 softmax(Q K^T / sqrt d) V for every query row (video and text)
+ * of every head; `out` is fp64 [heads][T][d] (device).  Used by the harness
+ * core (run_variants) to score the variants as the reference does. */
+size_t rsa_dense_reference_scratch_size(const rsa_shape* shape);
+rsa_status rsa_dense_reference(const rsa_shape* shape, const void* q, const void* k, const void* v,
+                               double* out, void* scratch, void* stream);
+
 /* Synchronises `stream` and converts device-side status flags (e.g. a
  * reallocation denominator <= 0, ipar.py:62-64) into an rsa_status. */
 rsa_status rsa_check_device_status(void* workspace, void* stream);

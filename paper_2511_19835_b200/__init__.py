@@ -22,6 +22,7 @@ _LAZY = {"rectified_attention_pipeline", "block_sparse_attention", "text_full_at
          "rectified_sparse_attention"}
 _REORDER = {"morton_permutation", "reorder_morton", "inverse_permutation"}
 _DIAG = {"gain_error", "gapr_condition_agreement", "denominator_equivalence_report"}
+_HARNESS = {"run_variants", "full_attention_reference", "normalized_l1", "cosine_similarity", "AlignmentReport"}
 
 
 def __getattr__(name):
@@ -35,4 +36,7 @@ def __getattr__(name):
     if name in _DIAG:
         from . import diagnostics
         return getattr(diagnostics, name)
+    if name in _HARNESS:
+        from . import harness
+        return getattr(harness, name)
     raise AttributeError(name)

@@ -457,6 +457,24 @@ rsa_status rsa_diagnostics(const rsa_shape* shape, const void* q, const void* k,
   return RSA_OK;
 }
 
+size_t rsa_dense_reference_scratch_size(const rsa_shape* shape) {
+  rsa::Geometry g;
+  if (make_geometry(shape, &g) != RSA_OK) return 0;
+  return rsa::dense_scratch_size(g);
+}
+
+rsa_status rsa_dense_reference(const rsa_shape* shape, const void* q, const void* k, const void* v, double* out,
+                               void* scratch, void* stream) {
+  g_launches = 0;
+  rsa::Geometry g;
+  rsa_status s = make_geometry(shape, &g);
+  if (s != RSA_OK) return s;
+  if (!q || !k || !v || !out || !scratch) return fail(RSA_ERR_SHAPE, "null pointer");
+  cudaError_t e = rsa::launch_dense_reference(g, q, k, v, out, scratch, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "dense_reference");
+  return RSA_OK;
+}
+
 rsa_status rsa_check_device_status(void* workspace, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int32_t flags[4] = {0, 0, 0, 0};

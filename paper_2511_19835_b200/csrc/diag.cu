@@ -151,6 +151,27 @@ __global__ void __launch_bounds__(DT) diag_err_kernel(const double* __restrict__
   if (threadIdx.x == 0) exact_error[(h * g.N + n) * g.M + m] = tot;
 }
 
+// softmax rows in place: W = exp(S/sqrt d - max) / sum  (core.py:204-208, 223-224)
+__global__ void __launch_bounds__(DT) softmax_rows_kernel(double* __restrict__ S, int64_t T, double sqrt_d) {
+  __shared__ double red[DT / 32];
+  double* row = S + (int64_t)blockIdx.x * T;
+  double mx = -DBL_MAX;
+  for (int64_t j = threadIdx.x; j < T; j += DT) {
+    const double s = row[j] / sqrt_d;
+    row[j] = s;
+    mx = fmax(mx, s);
+  }
+  mx = block_reduce_max(mx, red);
+  double part = 0.0;
+  for (int64_t j = threadIdx.x; j < T; j += DT) {
+    const double e = exp(row[j] - mx);
+    row[j] = e;
+    part += e;
+  }
+  const double sum = block_reduce_sum(part, red);
+  for (int64_t j = threadIdx.x; j < T; j += DT) row[j] = row[j] / sum;
+}
+
 cublasHandle_t diag_cublas() {
   static thread_local cublasHandle_t handles[64] = {};
   int dev = 0;
@@ -207,6 +228,51 @@ cudaError_t launch_diagnostics(const Geometry& g, const void* q, const void* k, 
                                                       sqrt_d);
       diag_err_kernel<<<dim3((unsigned)g.M, (unsigned)cn), DT, 0, st>>>(S, g, h, n0, rmax, rsum, a_tok,
                                                                        exact_error, sqrt_d);
+    }
+  }
+  return cudaGetLastError();
+}
+
+size_t dense_scratch_size(const Geometry& g) {
+  const int64_t nc = diag_chunk_blocks(g);
+  return (size_t)(3 * g.T * g.d + nc * g.B * g.T) * 8 + 1024;
+}
+
+// Dense fp64 attention of every query row (video and text) over all keys:
+// the reference's ground truth full_attention_oracle (core.py:211-225).
+cudaError_t launch_dense_reference(const Geometry& g, const void* q, const void* k, const void* v, double* out,
+                                   void* scratch, cudaStream_t st) {
+  cublasHandle_t hb = diag_cublas();
+  if (!hb || cublasSetStream(hb, st) != CUBLAS_STATUS_SUCCESS) return cudaErrorInitializationError;
+  const int64_t rows_per = diag_chunk_blocks(g) * g.B;
+  double* k64 = static_cast<double*>(scratch);
+  double* v64 = k64 + g.T * g.d;
+  double* q64 = v64 + g.T * g.d;
+  double* W = q64 + g.T * g.d;
+  const double sqrt_d = sqrt((double)g.d);
+  const size_t esz = g.dtype == RSA_BF16 ? 2 : g.dtype == RSA_F32 ? 4 : 8;
+  auto convert = [&](const void* src, double* dst, int64_t n) {
+    const unsigned blocks = (unsigned)((n + 255) / 256);
+    if (g.dtype == RSA_BF16) to_f64_kernel<<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(src), dst, n);
+    else if (g.dtype == RSA_F32) to_f64_kernel<<<blocks, 256, 0, st>>>(static_cast<const float*>(src), dst, n);
+    else to_f64_kernel<<<blocks, 256, 0, st>>>(static_cast<const double*>(src), dst, n);
+  };
+  for (int64_t h = 0; h < g.H; ++h) {
+    const size_t off = (size_t)h * g.T * g.d * esz;
+    convert(static_cast<const char*>(k) + off, k64, g.T * g.d);
+    convert(static_cast<const char*>(v) + off, v64, g.T * g.d);
+    convert(static_cast<const char*>(q) + off, q64, g.T * g.d);
+    for (int64_t r0 = 0; r0 < g.T; r0 += rows_per) {
+      const int64_t rows = std::min(rows_per, g.T - r0);
+      const double one = 1.0, zero = 0.0;
+      if (cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, (int)g.T, (int)rows, (int)g.d, &one, k64, (int)g.d,
+                      q64 + r0 * g.d, (int)g.d, &zero, W, (int)g.T) != CUBLAS_STATUS_SUCCESS)
+        return cudaErrorUnknown;
+      softmax_rows_kernel<<<(unsigned)rows, DT, 0, st>>>(W, g.T, sqrt_d);
+      // out rows (row-major rows x d) = W (rows x T) . V (T x d)
+      if (cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)g.d, (int)rows, (int)g.T, &one, v64, (int)g.d, W,
+                      (int)g.T, &zero, out + (h * g.T + r0) * g.d, (int)g.d) != CUBLAS_STATUS_SUCCESS)
+        return cudaErrorUnknown;
     }
   }
   return cudaGetLastError();

@@ -90,6 +90,9 @@ cudaError_t launch_attn_simt(const Geometry& g, const void* q, const void* k, co
 bool tc_supported(const Geometry& g);
 void morton_permutation_host(int64_t t, int64_t h, int64_t w, int32_t* perm);
 size_t diag_scratch_size(const Geometry& g);
+size_t dense_scratch_size(const Geometry& g);
+cudaError_t launch_dense_reference(const Geometry& g, const void* q, const void* k, const void* v, double* out,
+                                   void* scratch, cudaStream_t st);
 cudaError_t launch_diagnostics(const Geometry& g, const void* q, const void* k, const Workspace& ws,
                                double* gain, double* error, double* exact_gain, double* exact_error,
                                double* s_sum, double* s_sum_pool, void* scratch, cudaStream_t st);

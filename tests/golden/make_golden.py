@@ -251,7 +251,32 @@ def rsat_goldens(rt) -> None:
     np.savez_compressed(HERE / "rsat_files.npz", **out)
 
 
+HARNESS_CASES = ((21, 128, 20, 16, 16, 0.25), (22, 256, 0, 32, 32, 0.1))
+
+
+def harness_goldens(rt) -> None:
+    """rectattn.harness.run_variants (harness.py:177-220) on small fp64 problems."""
+    from oracle import rsa_oracle as O
+    from rectattn.harness import run_variants
+    out = {}
+    for seed, t_v, t_t, d, b, f in HARNESS_CASES:
+        qv, qt, k, v = O.random_problem(seed, t_v=t_v, t_t=t_t, d=d)
+        prob = rt.AttentionProblem(q_video=qv, q_text=qt, k=k, v=v, d=d, block=b)
+        reps = run_variants(prob, rt.SparsityConfig(f, 0.0, 0, False), rt.VARIANTS)
+        for name, r in reps.items():
+            tag = f"s{seed}_{name}"
+            out[tag] = np.array([r.normalized_l1, r.cosine_similarity, r.sparsity, r.flops_full,
+                                 r.flops_sparse, r.flops_overhead,
+                                 np.nan if r.gapr_agreement is None else r.gapr_agreement, float(r.checks_passed)])
+    np.savez_compressed(HERE / "harness_variants.npz", **out)
+
+
 def main():
+    if "--harness-only" in sys.argv:
+        sys.path.insert(0, "/root/reference/pkg/src")
+        import rectattn as rt
+        harness_goldens(rt)
+        return
     if "--rsat-only" in sys.argv:
         sys.path.insert(0, "/root/reference/pkg/src")
         import rectattn as rt
@@ -275,6 +300,7 @@ def main():
         morton_goldens(rt)
         diag_goldens(rt)
         rsat_goldens(rt)
+        harness_goldens(rt)
         if "--no-large" not in sys.argv:
             large_goldens(rt)
     (HERE / "README.md").write_text(
