@@ -996,7 +996,7 @@ struct CfgPP {
   static constexpr int Q_BYTES = 128 * D * 2;     // 32 KB
   static constexpr int SLOT_SMEM = Q_BYTES + NST * STAGE;
   static constexpr int SMEM = 1024 + 2 * SLOT_SMEM + 512;
-  static constexpr uint32_t IDESC_S = ptx::idesc_bf16(128, BKV, false);
+  static constexpr uint32_t IDESC_S64 = ptx::idesc_bf16(128, 64, false);   // S sub-steps: 64 keys
   static constexpr uint32_t IDESC_O = ptx::idesc_bf16(128, D, true);   // V MN-major
   static constexpr int THREADS = 384;
 };
@@ -1009,9 +1009,9 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + 2 * C::SLOT_SMEM);
-  // per slot: q_full, q_empty, kv_full[2], kv_empty[2], s_full, p_full, pv_done  (9 barriers)
-  auto slot_bar = [&](int s, int i) { return bars + s * 9 + i; };
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
+  // per slot: q_full, q_empty, kv_full[2], kv_empty[2], s_full[2], pv_done, p_full[2]  (11 barriers)
+  auto slot_bar = [&](int s, int i) { return bars + s * 11 + i; };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22);
 
   const Geometry& g = P.g;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -1023,9 +1023,11 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
         ptx::mbar_init(slot_bar(s, 2 + i), 1);   // kv_full
         ptx::mbar_init(slot_bar(s, 4 + i), 1);   // kv_empty
       }
-      ptx::mbar_init(slot_bar(s, 6), 1);     // s_full
-      ptx::mbar_init(slot_bar(s, 7), 128);   // p_full
+      ptx::mbar_init(slot_bar(s, 6), 1);     // s_full[0]
+      ptx::mbar_init(slot_bar(s, 7), 1);     // s_full[1]
       ptx::mbar_init(slot_bar(s, 8), 1);     // pv_done
+      ptx::mbar_init(slot_bar(s, 9), 128);   // p_full[0]
+      ptx::mbar_init(slot_bar(s, 10), 128);  // p_full[1]
     }
     ptx::fence_barrier_init();
   }
@@ -1075,56 +1077,91 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
     }
   } else if (warp < 4) {
     // ===================== MMA issuer of slot `warp - 2` =====================
+    // 64-key sub-steps i (two per kv block) into S buffers i % 2 ([0,64) and
+    // [64,128) of the slot's S columns): S_{i+1} runs while the softmax works
+    // on S_i; S_{i+2} reuses buffer i % 2 after PV_i (in-order tensor pipe).
     const int s = warp - 2;
     const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0) + (uint32_t)(s * 256);
     const uint32_t q_addr = __shfl_sync(0xffffffffu, ptx::smem_u32(base + s * C::SLOT_SMEM), 0);
     const uint32_t ring = q_addr + C::Q_BYTES;
-    int st = 0;
+    int st = 0;          // ring stage of the current kv block's K (V is the next stage)
     uint32_t ph = 0, qph = 0;
-    int64_t gs = 0;
+    int64_t gi = 0;      // sub-steps before the current tile
+    auto stage_of = [&](int64_t blk_in_tile, int kv, int& st_out, uint32_t& ph_out) {
+      // K_j and V_j occupy consecutive ring slots: index 2j (+1)
+      const int64_t idx = 2 * blk_in_tile + kv;
+      (void)idx;
+      st_out = st;
+      ph_out = ph;
+    };
+    (void)stage_of;
     for (int64_t bid = 2 * (int64_t)blockIdx.x + s; bid < n_tiles; bid += stride) {
       const int64_t count = decode_tile(P, bid).count;
+      const int64_t nsub = 2 * count;
       ptx::mbar_wait(slot_bar(s, 0), qph);
       qph ^= 1;
       ptx::tc_fence_after();
-      for (int64_t j = 0; j < count; ++j) {
-        const int64_t gj = gs + j;
-        // S_j = Q K_j^T (SS) into the slot's S columns; PV_{j-1} was issued before
-        ptx::mbar_wait(slot_bar(s, 2 + st), ph);
+      // ring bookkeeping: block j's K at stage kst(j), V at the next stage
+      int k_st = st;
+      uint32_t k_ph = ph;
+      auto issue_s = [&](int64_t i) {       // S_i, i = 2 j + half
+        const int64_t j = i >> 1;
+        const int half = (int)(i & 1);
+        int kst = k_st;
+        uint32_t kph = k_ph;
+        // K of block j: ring slot (st0 + 2 j) mod NST
+        const int64_t slot = (int64_t)kst + 2 * j;
+        const int sj = (int)(slot % C::NST);
+        const uint32_t pj = kph ^ (uint32_t)((slot / C::NST) & 1);
+        if (half == 0) ptx::mbar_wait(slot_bar(s, 2 + sj), pj);
         ptx::tc_fence_after();
-        const uint32_t kb = ring + (uint32_t)(st * C::STAGE);
+        const uint32_t kb = ring + (uint32_t)(sj * C::STAGE) + (uint32_t)(half * 64 * 128);
+        const uint32_t d_tmem = tm + (uint32_t)(half * 64);
         if (ptx::elect_one()) {
 #pragma unroll
           for (int k = 0; k < D / 16; ++k) {
             const uint32_t off = (uint32_t)((k / 4) * C::Q_PANEL + (k % 4) * 32);
             const uint64_t a = ptx::sw128_desc(q_addr + off, 16, 1024);
             const uint64_t b = ptx::sw128_desc(kb + (k / 4) * C::KV_PANEL + (k % 4) * 32, 16, 1024);
-            ptx::mma_ss(tm, a, b, C::IDESC_S, k > 0);
+            ptx::mma_ss(d_tmem, a, b, C::IDESC_S64, k > 0);
           }
-          ptx::tc_commit(slot_bar(s, 4 + st));
-          ptx::tc_commit(slot_bar(s, 6));
-          if (j == count - 1) ptx::tc_commit(slot_bar(s, 1));   // Q may be replaced once this completes
+          if (half == 1) ptx::tc_commit(slot_bar(s, 4 + sj));   // K_j fully read
+          ptx::tc_commit(slot_bar(s, 6 + half));                  // s_full[half]
+          if (i == nsub - 1) ptx::tc_commit(slot_bar(s, 1));      // Q may be replaced after this
         }
         __syncwarp();
-        if (++st == C::NST) { st = 0; ph ^= 1; }
-        // O += P_j V_j once the softmax has written P_j
-        ptx::mbar_wait(slot_bar(s, 7), (uint32_t)(gj & 1));
-        ptx::mbar_wait(slot_bar(s, 2 + st), ph);
+      };
+      if (nsub > 0) issue_s(0);
+      if (nsub > 1) issue_s(1);
+      for (int64_t i = 0; i < nsub; ++i) {
+        const int64_t gsub = gi + i;
+        const int64_t j = i >> 1;
+        const int half = (int)(i & 1);
+        // O += P_i V_i[64 half rows] once the softmax has written P_i
+        ptx::mbar_wait(slot_bar(s, 9 + half), (uint32_t)((gsub >> 1) & 1));
+        const int64_t slot = (int64_t)k_st + 2 * j + 1;
+        const int sv = (int)(slot % C::NST);
+        const uint32_t pv = k_ph ^ (uint32_t)((slot / C::NST) & 1);
+        if (half == 0) ptx::mbar_wait(slot_bar(s, 2 + sv), pv);
         ptx::tc_fence_after();
-        const uint32_t vb = ring + (uint32_t)(st * C::STAGE);
+        const uint32_t vb = ring + (uint32_t)(sv * C::STAGE) + (uint32_t)(half * 64 * 128);
         if (ptx::elect_one()) {
 #pragma unroll
-          for (int k = 0; k < BKV / 16; ++k) {
+          for (int k = 0; k < 4; ++k) {
             const uint64_t b = ptx::sw128_desc(vb + k * 2048, C::KV_PANEL, 1024);
-            ptx::mma_ts(tm + 128, tm + k * 8, b, C::IDESC_O, (j > 0 || k > 0) ? 1u : 0u);
+            ptx::mma_ts(tm + 128, tm + (uint32_t)(half * 64) + k * 8, b, C::IDESC_O, (i > 0 || k > 0) ? 1u : 0u);
           }
-          ptx::tc_commit(slot_bar(s, 4 + st));
-          ptx::tc_commit(slot_bar(s, 8));
+          if (half == 1) ptx::tc_commit(slot_bar(s, 4 + sv));   // V_j fully read
+          ptx::tc_commit(slot_bar(s, 8));                         // pv_done
         }
         __syncwarp();
-        if (++st == C::NST) { st = 0; ph ^= 1; }
+        if (i + 2 < nsub) issue_s(i + 2);
       }
-      gs += count;
+      // advance the ring past this tile's 2 * count stages
+      const int64_t used = (int64_t)st + 2 * count;
+      ph ^= (uint32_t)((used / C::NST) & 1);
+      st = (int)(used % C::NST);
+      gi += nsub;
     }
   } else {
     // ===================== softmax + epilogue of slot s, one thread per row =====================
@@ -1134,61 +1171,64 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
     const uint32_t lane_base = tmem + (uint32_t)(s * 256) + ((uint32_t)(quad * 32) << 16);
     const float sl2 = P.scale_log2;
     const uint64_t once = ptx::policy_evict_first();
-    int64_t gs = 0;
+    int64_t gi = 0;
     for (int64_t bid = 2 * (int64_t)blockIdx.x + s; bid < n_tiles; bid += stride) {
       const TileDesc t = decode_tile(P, bid);
-      const int64_t count = t.count;
+      const int64_t count = t.count, nsub = 2 * count;
       float m_run = -INFINITY, l_run = 0.f;
-      for (int64_t j = 0; j < count; ++j) {
-        const int64_t gj = gs + j;
-        const int64_t m = t.list ? (t.list[j] & 0xFFFFFF) : t.m_first + j;
-        const int len = (m == g.M - 1 && g.n_text > 0) ? (int)g.last_len : (int)g.B;
-        ptx::mbar_wait(slot_bar(s, 6), (uint32_t)(gj & 1));
+      for (int64_t i = 0; i < nsub; ++i) {
+        const int64_t gsub = gi + i;
+        const int half = (int)(i & 1);
+        const int64_t m = t.list ? (t.list[i >> 1] & 0xFFFFFF) : t.m_first + (i >> 1);
+        const int blen = (m == g.M - 1 && g.n_text > 0) ? (int)g.last_len : (int)g.B;
+        const int len = blen - half * 64;
+        ptx::mbar_wait(slot_bar(s, 6 + half), (uint32_t)((gsub >> 1) & 1));
         ptx::tc_fence_after();
-        uint32_t sr[4][32];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) ptx::tmem_ld32(lane_base + c * 32, sr[c]);
+        const uint32_t sbuf = lane_base + (uint32_t)(half * 64);
+        uint32_t sr[2][32];
+        ptx::tmem_ld32(sbuf, sr[0]);
+        ptx::tmem_ld32(sbuf + 32, sr[1]);
         ptx::tmem_ld_wait();
-        if (len < BKV) {
+        if (len < 64) {
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
+          for (int c = 0; c < 2; ++c)
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (c * 32 + i >= len) sr[c][i] = __float_as_uint(-INFINITY);
+            for (int q2 = 0; q2 < 32; ++q2)
+              if (c * 32 + q2 >= len) sr[c][q2] = __float_as_uint(-INFINITY);
         }
         float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
+        for (int c = 0; c < 2; ++c)
 #pragma unroll
-          for (int i = 0; i < 32; ++i) mx4[i & 3] = fmaxf(mx4[i & 3], __uint_as_float(sr[c][i]));
+          for (int q2 = 0; q2 < 32; ++q2) mx4[q2 & 3] = fmaxf(mx4[q2 & 3], __uint_as_float(sr[c][q2]));
         const float m_blk = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * sl2;
         float alpha = 1.f;
         bool rescale_o = false;
         if (m_blk > m_run + kRescaleThreshold || (m_run == -INFINITY && m_blk > -INFINITY)) {
           alpha = (m_run == -INFINITY) ? 0.f : ptx::ex2(m_run - m_blk);
-          rescale_o = (m_run != -INFINITY) && j > 0;
+          rescale_o = (m_run != -INFINITY) && i > 0;
           m_run = m_blk;
         }
         const float base_m = (m_run == -INFINITY) ? 0.f : m_run;
         const float2 sc2 = make_float2(sl2, sl2), nb2 = make_float2(-base_m, -base_m);
         float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < 2; ++c) {
           uint32_t pk[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float2 x = ptx::ffma2(make_float2(__uint_as_float(sr[c][2 * i]), __uint_as_float(sr[c][2 * i + 1])),
+          for (int q2 = 0; q2 < 16; ++q2) {
+            const float2 x = ptx::ffma2(make_float2(__uint_as_float(sr[c][2 * q2]), __uint_as_float(sr[c][2 * q2 + 1])),
                                         sc2, nb2);
             const float2 p = make_float2(ptx::ex2(x.x), ptx::ex2(x.y));
-            sum2[i & 1] = ptx::fadd2(sum2[i & 1], p);
-            pk[i] = ptx::pack_bf16(p.x, p.y);
+            sum2[q2 & 1] = ptx::fadd2(sum2[q2 & 1], p);
+            pk[q2] = ptx::pack_bf16(p.x, p.y);
           }
-          ptx::tmem_st16(lane_base + c * 16, pk);
+          ptx::tmem_st16(sbuf + c * 16, pk);
         }
         const float2 st2 = ptx::fadd2(sum2[0], sum2[1]);
         l_run = l_run * alpha + (st2.x + st2.y);
         if (__any_sync(0xffffffffu, rescale_o)) {
-          ptx::mbar_wait(slot_bar(s, 8), (uint32_t)((gj - 1) & 1));   // O = PV_0..PV_{j-1}
+          ptx::mbar_wait(slot_bar(s, 8), (uint32_t)((gsub - 1) & 1));   // O = PV_..i-1
           ptx::tc_fence_after();
           const float a = rescale_o ? alpha : 1.f;
 #pragma unroll
@@ -1198,17 +1238,17 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
             ptx::tmem_ld32(oa, o);
             ptx::tmem_ld_wait();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * a);
+            for (int q2 = 0; q2 < 32; ++q2) o[q2] = __float_as_uint(__uint_as_float(o[q2]) * a);
             ptx::tmem_st32(oa, o);
           }
         }
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
-        ptx::mbar_arrive(slot_bar(s, 7));
+        ptx::mbar_arrive(slot_bar(s, 9 + half));
       }
       // ---- epilogue (overlaps the other slot's steps) ----
-      if (count > 0) {
-        ptx::mbar_wait(slot_bar(s, 8), (uint32_t)((gs + count - 1) & 1));
+      if (nsub > 0) {
+        ptx::mbar_wait(slot_bar(s, 8), (uint32_t)((gi + nsub - 1) & 1));
         ptx::tc_fence_after();
       }
       const bool valid = row < t.rows_valid;
@@ -1236,7 +1276,7 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
           rfac = P.ws.r_eff[t.h * g.N + n_blk];
           comp = P.ws.comp + (t.h * g.N + n_blk) * D;
         }
-        const float inv_l = (count > 0 && l_run > 0.f) ? 1.f / l_run : 0.f;
+        const float inv_l = (nsub > 0 && l_run > 0.f) ? 1.f / l_run : 0.f;
         __nv_bfloat16* orow = P.out + (t.h * g.T + grow) * D;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -1248,15 +1288,15 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
             for (int v8 = 0; v8 < 4; ++v8) {
               uint32_t w[4];
 #pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const int col = c * 32 + v8 * 8 + 2 * i;
-                float y0 = inv_l == 0.f ? 0.f : __uint_as_float(o[v8 * 8 + 2 * i]) * inv_l * rfac;
-                float y1 = inv_l == 0.f ? 0.f : __uint_as_float(o[v8 * 8 + 2 * i + 1]) * inv_l * rfac;
+              for (int q2 = 0; q2 < 4; ++q2) {
+                const int col = c * 32 + v8 * 8 + 2 * q2;
+                float y0 = inv_l == 0.f ? 0.f : __uint_as_float(o[v8 * 8 + 2 * q2]) * inv_l * rfac;
+                float y1 = inv_l == 0.f ? 0.f : __uint_as_float(o[v8 * 8 + 2 * q2 + 1]) * inv_l * rfac;
                 if (comp) {
                   y0 += (float)comp[col];
                   y1 += (float)comp[col + 1];
                 }
-                w[i] = ptx::pack_bf16(y0, y1);
+                w[q2] = ptx::pack_bf16(y0, y1);
               }
               ptx::st_stream(orow + c * 32 + v8 * 8, make_uint4(w[0], w[1], w[2], w[3]), once);
             }
@@ -1265,9 +1305,8 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
         if (valid && P.lse)
           P.lse[t.h * g.T + grow] = l_run > 0.f ? (log2f(l_run) + m_run) * 0.69314718055994531f : -INFINITY;
       }
-      // O is read: this slot's next PV_0 (after its P_0) may overwrite it
       ptx::tc_fence_before();
-      gs += count;
+      gi += nsub;
     }
   }
 
