@@ -33,7 +33,7 @@ namespace {
 // ----------------------------------------------------------------------------
 // block-wide deterministic reductions (fixed tree order)
 // ----------------------------------------------------------------------------
-constexpr int RT = 256;
+constexpr int RT = 128;
 
 __device__ __forceinline__ double warp_sum(double x) {
 #pragma unroll
