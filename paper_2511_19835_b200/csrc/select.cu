@@ -411,6 +411,308 @@ __global__ void __launch_bounds__(RT) select_rows_kernel(SelectParams P) {
   }
 }
 
+// ----------------------------------------------------------------------------
+// Register-resident select_rows (n_cols <= RT * PER, p == 0): same arithmetic,
+// element for element, as select_rows_kernel, with 32-bit indices, the row in
+// registers (strided for the softmax, blocked for the selection so ascending
+// index order is thread order), shuffle scans and one barrier per reduction.
+// ----------------------------------------------------------------------------
+constexpr int NW = RT / 32;
+
+template <typename F>
+__device__ __forceinline__ double block_reduce(double x, double* slot, F op) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = op(x, __shfl_xor_sync(0xffffffffu, x, o));
+  if ((threadIdx.x & 31) == 0) slot[threadIdx.x >> 5] = x;
+  __syncthreads();
+  double y = slot[0];
+#pragma unroll
+  for (int w = 1; w < NW; ++w) y = op(y, slot[w]);
+  return y;
+}
+
+// exclusive prefix of x over the block in thread order; *total = sum
+__device__ __forceinline__ int block_scan(int x, int* slot, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) slot[warp] = incl;
+  __syncthreads();
+  int before = 0, all = 0;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    const int c = slot[w];
+    before += w < warp ? c : 0;
+    all += c;
+  }
+  *total = all;
+  return before + incl - x;
+}
+
+// resident CTAs per SM the register budget is held to (8 at PER <= 10: measured
+// 1.07 vs 1.46 ms for the whole K2 at HunyuanVideo size with the compiler's 96 registers)
+constexpr int sel_min_blocks(int per) { return per <= 10 ? 8 : per <= 12 ? 6 : 4; }
+
+template <int PER>
+__global__ void __launch_bounds__(RT, sel_min_blocks(PER)) select_rows_reg_kernel(SelectParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int N = (int)P.g.N, M = (int)P.g.M, Tt = (int)P.g.Tt, n_cols = (int)P.g.n_cols;
+  const int B = (int)P.g.B, n_text = (int)P.g.n_text;
+  const int n_mix = N + Tt;
+  const int n = blockIdx.x, h = blockIdx.y;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const size_t row = (size_t)h * N + n;
+  double* sc = reinterpret_cast<double*>(smem_raw);   // [n_cols] scores / sqrt(d)
+  double* sa = sc + n_cols;                            // [n_mix] a_hat
+  double* at = sa + n_mix;                             // [n_text] text a_pool columns
+  uint8_t* sb = reinterpret_cast<uint8_t*>(at + n_text);  // [M] mask bits
+  __shared__ double red[6][NW];
+  __shared__ int ired[2][NW];
+  __shared__ unsigned hist[2][256];
+  __shared__ unsigned long long s_and[NW], s_or[NW];
+  __shared__ int sh_digit, sh_rem, sh_done;
+
+  for (int k = t; k < 256; k += RT) hist[0][k] = 0u;
+
+  // ---- scores / sqrt(d) and the IPAR softmax (ipar.py:36-42), strided ----
+  double* srow = P.ws.scores + row * n_cols;
+  double v[PER];
+  double mx = -DBL_MAX;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int j = t + i * RT;
+    v[i] = 0.0;
+    if (j < n_cols) {
+      const double s = srow[j] / P.sqrt_d;
+      srow[j] = s;
+      sc[j] = s;
+      v[i] = s;
+      if (j < n_mix) mx = fmax(mx, s);
+    }
+  }
+  mx = block_reduce(mx, red[0], [](double a, double b) { return fmax(a, b); });
+  double part = 0.0;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int j = t + i * RT;
+    if (j < n_mix) { v[i] = exp(v[i] - mx); part += v[i]; }
+  }
+  const auto add = [](double a, double b) { return a + b; };
+  const double tot = block_reduce(part, red[1], add);
+#pragma unroll
+  for (int i = 0; i < PER; ++i)
+    if (t + i * RT < n_mix) v[i] = v[i] / tot;
+  // ---- reallocation (ipar.py:45-66) ----
+  if (Tt > 0 && B > 1) {
+    double pv = 0.0, pt = 0.0;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int j = t + i * RT;
+      if (j < N) pv += v[i];
+      else if (j < n_mix) pt += v[i];
+    }
+    const double sum_v = block_reduce(pv, red[2], add);
+    const double sum_t = block_reduce(pt, red[3], add);
+    const double D = (double)B * sum_v + sum_t;
+    if (D <= 0.0 && t == 0) atomicOr(P.ws.status + ST_DEGENERATE, 1);
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int j = t + i * RT;
+      if (j < n_mix) v[i] = (j < N) ? ((double)B * v[i]) / D : v[i] / D;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < PER; ++i)
+    if (t + i * RT < n_mix) sa[t + i * RT] = v[i];
+  __syncthreads();
+  // ---- text re-aggregation (ipar.py:76-83): one warp per text block ----
+  for (int jt = warp; jt < n_text; jt += NW) {
+    const int lo = N + jt * B, hi = min(lo + B, n_mix);
+    double pj = 0.0;
+    for (int i = lo + lane; i < hi; i += 32) pj += sa[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pj += __shfl_xor_sync(0xffffffffu, pj, o);
+    if (lane == 0) at[jt] = pj;
+  }
+  __syncthreads();
+  double* ap_out = P.ws.a_pool + row * M;
+  for (int m = t; m < M; m += RT) ap_out[m] = m < N ? sa[m] : at[m - N];
+
+  // ---- the a_pool row, blocked: thread t owns m = t * PER + i ----
+  const int m0 = t * PER;
+  double a[PER];
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int m = m0 + i;
+    a[i] = m < M ? (m < N ? sa[m] : at[m - N]) : 0.0;
+  }
+  uint8_t b[PER];
+  if (P.variant == RSA_VARIANT_FULL) {
+#pragma unroll
+    for (int i = 0; i < PER; ++i) b[i] = BIT_MASK | BIT_IMPORTANCE;
+  } else {
+    // exact top-K by MSB-first radix select on the fp64 bit patterns, ties by
+    // ascending index (see select_rows_kernel)
+    const int K = (int)(P.k_floor < M ? P.k_floor : M);
+    uint64_t k_and = ~0ull, k_or = 0ull;
+#pragma unroll
+    for (int i = 0; i < PER; ++i)
+      if (m0 + i < M) {
+        const uint64_t key = (uint64_t)__double_as_longlong(a[i]);
+        k_and &= key;
+        k_or |= key;
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      k_and &= __shfl_xor_sync(0xffffffffu, k_and, o);
+      k_or |= __shfl_xor_sync(0xffffffffu, k_or, o);
+    }
+    if (lane == 0) { s_and[warp] = k_and; s_or[warp] = k_or; }
+    __syncthreads();
+    k_and = ~0ull;
+    k_or = 0ull;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) { k_and &= s_and[w]; k_or |= s_or[w]; }
+    const uint64_t differ = k_and ^ k_or;
+    int top = 56;
+    while (top > 0 && ((differ >> top) & 0xFF) == 0) top -= 8;
+    uint64_t prefix = 0, pmask = 0;
+    if (top < 56) {
+      pmask = ~0ull << (top + 8);
+      prefix = k_and & pmask;
+    }
+    int remaining = K, hb = 0;
+    for (int shift = top; shift >= 0; shift -= 8) {
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        const uint64_t key = (uint64_t)__double_as_longlong(a[i]);
+        if (m0 + i < M && (key & pmask) == prefix) atomicAdd(&hist[hb][(key >> shift) & 0xFF], 1u);
+      }
+      for (int k = t; k < 256; k += RT) hist[hb ^ 1][k] = 0u;   // next pass's bins
+      __syncthreads();
+      if (warp == 0) {
+        unsigned c[8], cnt = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) { c[i] = hist[hb][255 - 8 * lane - i]; cnt += c[i]; }
+        unsigned incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const unsigned excl = incl - cnt;
+        if (excl < (unsigned)remaining && incl >= (unsigned)remaining) {
+          unsigned run = excl;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            if (run + c[i] >= (unsigned)remaining) {
+              sh_digit = 255 - 8 * lane - i;
+              sh_rem = remaining - (int)run;
+              sh_done = (run + c[i] == (unsigned)remaining);
+              break;
+            }
+            run += c[i];
+          }
+        }
+      }
+      __syncthreads();
+      prefix |= (uint64_t)sh_digit << shift;
+      pmask |= (uint64_t)0xFF << shift;
+      remaining = sh_rem;
+      hb ^= 1;
+      if (sh_done) break;
+    }
+    // keys > v* are in; the first `remaining` keys == v* in ascending index too
+    int eq = 0;
+#pragma unroll
+    for (int i = 0; i < PER; ++i)
+      eq += (m0 + i < M && ((uint64_t)__double_as_longlong(a[i]) & pmask) == prefix) ? 1 : 0;
+    int tot_eq;
+    int rank = block_scan(eq, ired[0], &tot_eq);
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int m = m0 + i;
+      const uint64_t key = (uint64_t)__double_as_longlong(a[i]) & pmask;
+      bool sel = false;
+      if (m < M) sel = key > prefix || (key == prefix && rank++ < remaining);
+      uint8_t bb = sel ? BIT_IMPORTANCE : 0;
+      const int dist = m > n ? m - n : n - m;
+      if (dist <= P.radius) bb |= BIT_ADJ;
+      if ((bb & (BIT_IMPORTANCE | BIT_ADJ)) || (P.force_text && M > N && m >= N)) bb |= BIT_MASK;
+      b[i] = bb;
+    }
+  }
+
+  // ---- R = 1 - excluded mass (rectify.py:56-63) ----
+  double ex = 0.0;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) ex += (m0 + i < M && !(b[i] & BIT_MASK)) ? a[i] : 0.0;
+  const double R = 1.0 - block_reduce(ex, red[4], add);
+
+  // ---- GAPR gate (masks.py:138-186) ----
+  const bool deficit = P.ws.status[ST_DEFICIT] != 0;
+  const int d = (int)P.g.d;
+  int kv_local = 0;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int m = m0 + i;
+    if (m >= M) continue;
+    const double len = (m < N) ? (double)B : (m == M - 1 ? (double)P.g.last_len : (double)B);
+    const double s = (m < N) ? sc[m] : sc[N + Tt + (m - N)];
+    const double gain = fabs(((double)B * len) * s);
+    double err = 0.0;
+    if (deficit) {
+      const int krow = (m < N) ? m : N + Tt + (m - N);
+      const double* kp = P.ws.k_cat + ((size_t)h * n_cols + krow) * d;
+      const double* kd = P.ws.k_def + ((size_t)h * M + m) * d;
+      const double* qp = P.ws.q_pool + row * d;
+      const double* qd = P.ws.q_def + row * d;
+      double d1 = 0.0, d2 = 0.0;
+      for (int c = 0; c < d; ++c) { d1 = fma(qd[c], kp[c], d1); d2 = fma(qp[c], kd[c], d2); }
+      const double t1 = (d1 * len) * P.inv_sqrt_d;
+      const double t2 = ((double)B * d2) * P.inv_sqrt_d;
+      err = fabs(t1 + t2);
+    }
+    uint8_t bb = b[i];
+    if (gain > err) bb |= BIT_COMP;
+    const bool masked = bb & BIT_MASK;
+    bool applied = false;
+    if (P.variant == RSA_VARIANT_SPARSE_RECTIFIED) applied = !masked && (bb & BIT_COMP);
+    else if (P.variant == RSA_VARIANT_COMPENSATE_ALL) applied = !masked;
+    if (applied) bb |= BIT_APPLIED;
+    sb[m] = bb;
+    kv_local += masked ? 1 : 0;
+    b[i] = bb;
+  }
+  // ---- ascending kv list (kernel.py:92 np.flatnonzero) ----
+  int total;
+  int off = block_scan(kv_local, ired[1], &total);   // its barrier also publishes sb
+  int32_t* list = P.ws.kv_list + row * M;
+#pragma unroll
+  for (int i = 0; i < PER; ++i)
+    if (m0 + i < M && (b[i] & BIT_MASK)) list[off++] = m0 + i;
+  uint8_t* bits_out = P.ws.mask_bits + row * M;
+  double* applied_out = P.ws.a_applied + row * M;   // operand of the compensation GEMM
+  for (int m = t; m < M; m += RT) {
+    const uint8_t bb = sb[m];
+    bits_out[m] = bb;
+    applied_out[m] = (bb & BIT_APPLIED) ? (m < N ? sa[m] : at[m - N]) : 0.0;
+  }
+  if (t == 0) {
+    P.ws.r[row] = R;
+    const bool rect = P.variant == RSA_VARIANT_SPARSE_RECTIFIED ||
+                      P.variant == RSA_VARIANT_SPARSE_RECTIFIED_NO_GAPR ||
+                      P.variant == RSA_VARIANT_COMPENSATE_ALL;
+    P.ws.r_eff[row] = rect ? (float)R : 1.0f;
+    P.ws.kv_count[row] = total;
+    if (total == 0) atomicOr(P.ws.status + ST_EMPTY_ROW, 1);
+  }
+}
+
 // kv lists from an explicit caller mask (kernel-only seam)
 __global__ void __launch_bounds__(RT) lists_from_mask_kernel(const uint8_t* __restrict__ mask,
                                                              Workspace ws, Geometry g) {
@@ -503,12 +805,37 @@ cudaError_t launch_select(const Geometry& g, const rsa_config& cfg, int64_t k_fl
   while (p2 < g.M) p2 <<= 1;
   P.p2 = p2;
   P.use_sort = 0;   // radix select (a full bitonic sort of every row measured 2x slower)
-  const size_t smem = (size_t)(g.N + g.Tt) * 8 + (size_t)g.M * 8 + (size_t)p2 * 12 + (size_t)g.M + 16;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(select_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // the register-resident kernel covers rows up to 16 * RT columns without the
+  // cumulative-weight rule (p > 0 needs the sorted cumsum); RSA_SELECT_REG=0 forces
+  // the general one (A/B)
+  static const int reg_env = [] { const char* e = getenv("RSA_SELECT_REG"); return e ? atoi(e) : 1; }();
+  const int per = (int)((g.n_cols + RT - 1) / RT);
+  const bool reg = reg_env != 0 && !(P.p > 0.0) && !P.use_sort && per <= 16;
+  if (reg) {
+    const size_t smem = (size_t)(g.n_cols + g.N + g.Tt + g.n_text) * 8 + (size_t)g.M + 16;
+    auto launch = [&](auto kern) -> cudaError_t {
+      if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+      }
+      kern<<<dim3((unsigned)g.N, (unsigned)g.H), RT, smem, st>>>(P);
+      return cudaSuccess;
+    };
+    cudaError_t e = per <= 4 ? launch(select_rows_reg_kernel<4>)
+                  : per <= 6 ? launch(select_rows_reg_kernel<6>)
+                  : per <= 8 ? launch(select_rows_reg_kernel<8>)
+                  : per <= 10 ? launch(select_rows_reg_kernel<10>)
+                  : per <= 12 ? launch(select_rows_reg_kernel<12>)
+                  : launch(select_rows_reg_kernel<16>);
     if (e != cudaSuccess) return e;
+  } else {
+    const size_t smem = (size_t)(g.N + g.Tt) * 8 + (size_t)g.M * 8 + (size_t)p2 * 12 + (size_t)g.M + 16;
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(select_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    select_rows_kernel<<<dim3((unsigned)g.N, (unsigned)g.H), RT, smem, st>>>(P);
   }
-  select_rows_kernel<<<dim3((unsigned)g.N, (unsigned)g.H), RT, smem, st>>>(P);
   ++*launches;
   // compensation rows: (a_pool masked to applied) @ v_pool   (rectify.py:84-87);
   // select_rows wrote the masked operand.  Row-major [N][d] = col-major d x N

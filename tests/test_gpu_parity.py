@@ -365,3 +365,29 @@ def test_tcgen05_persistent_many_tiles_per_cta():
     diff = (outs["tcgen05"][0].float() - outs["simt"][0].float()).abs().max().item()
     assert diff <= 1e-2, diff
     assert (outs["tcgen05"][1] - outs["simt"][1]).abs().max().item() <= 1e-2
+
+
+# ---------------------------------------------------------------- K2 row kernels
+
+@pytest.mark.parametrize("block,n_q,t_t,f,p,radius,force", [
+    (16, 1400, 20, 0.1, 0.0, 0, False),    # 1,422 score columns: 12 per thread
+    (24, 1700, 30, 0.3, 0.0, 2, True),     # 1,732 columns: 16 per thread; B=24 leaves pooling deficits
+    (24, 1700, 30, 0.1, 0.4, 1, False),    # p > 0: the general (sorted-cumsum) row kernel
+])
+def test_select_rows_wide_rows_vs_oracle(block, n_q, t_t, f, p, radius, force):
+    """K2 at row widths the HunyuanVideo shape does not reach (and a block size
+    with non-zero pooling deficits, so the GAPR error term is live): masks,
+    importance and the gain>error gate bit-exact, a_pool and R to 1e-12."""
+    d = 32
+    qv, qt, k, v = O.random_problem(7, t_v=block * n_q, t_t=t_t, d=d, dtype=np.float32)
+    res = run_np(qv, qt, k, v, block, f, p, radius, force, "sparse-rectified")
+    pooled = O.pool(qv, k, v, t_t, block)
+    imp = O.implicit_attention(pooled, d, block, t_t)
+    sel = O.select_mask(imp["a_pool"], f, p, radius, force, pooled["n_q"])
+    comp = O.gain(O.pooled_scores(pooled, d), block, pooled["lens"]) > \
+        O.pooling_error(qv, k, pooled, block, d)
+    np.testing.assert_array_equal(res.sparse_mask.mask, sel["mask"])
+    np.testing.assert_array_equal(res.sparse_mask.importance, sel["importance"])
+    np.testing.assert_array_equal(res.comp_mask.mask, comp)
+    np.testing.assert_allclose(res.implicit.a_pool, imp["a_pool"], atol=1e-12, rtol=0)
+    np.testing.assert_allclose(res.factors.r, O.rect_factors(imp["a_pool"], sel["mask"]), atol=1e-12, rtol=0)
