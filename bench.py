@@ -46,6 +46,10 @@ CONFIGS = {
                label="HunyuanVideo 720p x 129f attention (T_v 118,800 -> 118,784)"),
     "wan": dict(heads=40, t_v=75520, t_t=0, d=128, block=128, grid=(59, 32, 40),
                 label="Wan 2.1 14B 720p x 81f self-attention (T_v 75,600 -> 75,520)"),
+    # the exact HunyuanVideo token count: 928 full blocks + a ragged 16-token block
+    # (ragged_video extension; the reference raises BlockSizeError here)
+    "hv_exact": dict(heads=24, t_v=118800, t_t=256, d=128, block=128, grid=(33, 45, 80), ragged=True,
+                     label="HunyuanVideo 720p x 129f attention, exact T_v 118,800 (ragged final video block)"),
     "cfg1": dict(heads=2, t_v=3840, t_t=256, d=64, block=64, grid=(1, 60, 64),
                  label="synthetic B=1 H=2 N=4096 d=64 block=64 (reference CPU case)"),
 }
@@ -152,7 +156,7 @@ def synth_inputs(torch, cfg, heads, seed, device):
     g = torch.Generator(device=device).manual_seed(seed)
     t_v, t_t, d, B = cfg["t_v"], cfg["t_t"], cfg["d"], cfg["block"]
     T = t_v + t_t
-    nb = t_v // B
+    nb = -(-t_v // B)   # (a ragged final block keeps a partial run of its block mean)
     # 3-D sinusoidal positional embedding of the (t, h, w) grid (harness.py:69-89)
     t_, h_, w_ = cfg["grid"]
     d_hw = d // 3
@@ -174,8 +178,8 @@ def synth_inputs(torch, cfg, heads, seed, device):
     k = torch.empty_like(q)
     v = torch.empty_like(q)
     for h in range(heads):
-        qb = torch.randn(nb, d, generator=g, device=device).repeat_interleave(B, 0)
-        kb = torch.randn(nb, d, generator=g, device=device).repeat_interleave(B, 0)
+        qb = torch.randn(nb, d, generator=g, device=device).repeat_interleave(B, 0)[:t_v]
+        kb = torch.randn(nb, d, generator=g, device=device).repeat_interleave(B, 0)[:t_v]
         q[h, :t_v] = (qb + 0.3 * torch.randn(t_v, d, generator=g, device=device) + pos).bfloat16()
         k[h, :t_v] = (kb + 0.3 * torch.randn(t_v, d, generator=g, device=device) + pos).bfloat16()
         if t_t:
@@ -210,7 +214,17 @@ def cpu_reference_sample(cfg, f, variant, sample_blocks, seed=42):
 
 def _cpu_reference_sample(np, O, cfg, f, variant, sample_blocks, seed):
     t_v, t_t, d, B = cfg["t_v"], cfg["t_t"], cfg["d"], cfg["block"]
-    if t_t:
+    ragged = cfg.get("ragged", False)
+    if t_t and ragged:
+        # gen_synthetic needs full blocks: full-block problem + N(0,1) rows for the ragged block
+        tf = (t_v // B) * B
+        qv, qt, k, v = O.gen_synthetic(seed, tf, t_t, d, B, (1, tf // B, B), 1.0, 2.0, 0.3)
+        rng = np.random.default_rng(seed)
+        ex = [rng.standard_normal((t_v - tf, d)).astype(np.float32) for _ in range(3)]
+        qv = np.concatenate([qv, ex[0]])
+        k = np.concatenate([k[:tf], ex[1], k[tf:]])
+        v = np.concatenate([v[:tf], ex[2], v[tf:]])
+    elif t_t:
         qv, qt, k, v = O.gen_synthetic(seed, t_v, t_t, d, B, cfg["grid"], 1.0, 2.0, 0.3)
     else:
         rng = np.random.default_rng(seed)
@@ -218,10 +232,10 @@ def _cpu_reference_sample(np, O, cfg, f, variant, sample_blocks, seed):
         qt = np.zeros((0, d), np.float32)
     qv, qt, k, v = (O.round_to_bf16(x) for x in (qv, qt, k, v))
     t0 = time.perf_counter()
-    pooled = O.pool(qv, k, v, t_t, B)
+    pooled = O.pool(qv, k, v, t_t, B, ragged)
     imp = O.implicit_attention(pooled, d, B, t_t)
     scores = O.pooled_scores(pooled, d)
-    g = O.gain(scores, B, pooled["lens"])
+    g = O.gain(scores, B, pooled["lens"], pooled["q_lens"])
     e = O.pooling_error(qv, k, pooled, B, d)
     sel = O.select_mask(imp["a_pool"], f, 0.0, 0, False, pooled["n_q"])
     _ = g > e
@@ -304,7 +318,8 @@ def run_ours(args):
     heads = per[rank]
     q, k, v = synth_inputs(torch, cfg, heads, 1234 + lo, dev)
     T, d = q.shape[1], q.shape[2]
-    shape = nat.make_shape(heads, cfg["t_v"], cfg["t_t"], d, cfg["block"], "bfloat16", args.kernel)
+    shape = nat.make_shape(heads, cfg["t_v"], cfg["t_t"], d, cfg["block"], "bfloat16", args.kernel,
+                           ragged_video=cfg.get("ragged", False))
     conf = nat.make_config(f, 0.0, 0, False, args.variant)
     grid = nat.plan(shape, conf)
     ws = workspace_for(shape, dev)
@@ -368,8 +383,12 @@ def run_ours(args):
     lens = torch.full((grid.n_kv,), cfg["block"], dtype=torch.int64, device=dev)
     if grid.n_text_blocks:
         lens[-1] = grid.last_text_block_len
-    retained_tokens = int((mask * lens[None, None, :]).sum().item())
-    flops_video = 4 * cfg["block"] * d * retained_tokens
+    lens[grid.n_q - 1] = grid.last_video_block_len           # (a ragged final video block)
+    qlens = torch.full((grid.n_q,), cfg["block"], dtype=torch.int64, device=dev)
+    qlens[-1] = grid.last_video_block_len
+    # sum over query blocks of (query rows x retained kv tokens)
+    retained_pairs = int((mask * lens[None, None, :] * qlens[None, :, None]).sum().item())
+    flops_video = 4 * d * retained_pairs
     flops_text = 4 * cfg["t_t"] * T * d * heads
     flops_exec = flops_video + flops_text
     flops_dense = 4 * T * T * d * heads
@@ -420,7 +439,8 @@ def run_ours(args):
             out_box[:] = [rsa.rectified_sparse_attention(hq[None], hk[None], hv[None], num_text_tokens=cfg["t_t"],
                                                          block=cfg["block"], top_k_fraction=f,
                                                          variant=args.variant, kernel=args.kernel,
-                                                         workspace=ws, heads_per_chunk=args.e2e_chunk)]
+                                                         workspace=ws, heads_per_chunk=args.e2e_chunk,
+                                                         ragged_video=cfg.get("ragged", False))]
 
         e2e_step()
         e2e_step()   # second warm-up: the pinned output buffers come from torch's host cache from here on

@@ -52,14 +52,23 @@ typedef enum {
  * block/head_dim in {64,128}, the CUDA-core kernel otherwise. */
 typedef enum { RSA_KERNEL_AUTO = 0, RSA_KERNEL_TCGEN05 = 1, RSA_KERNEL_SIMT = 2 } rsa_kernel;
 
+/* rsa_shape.flags */
+#define RSA_SHAPE_RAGGED_VIDEO 1  /* allow T_v % block != 0: the final video block holds
+                                     T_v - (N-1)*block tokens (extension, SURVEY.md 8f
+                                     row 4; the reference raises BlockSizeError,
+                                     core.py:71-72).  Not accepted by the diagnostics. */
+
 typedef struct {
   int64_t heads;        /* independent (batch, head) problems                */
-  int64_t t_video;      /* T_v, must be a multiple of block (core.py:71-72)    */
+  int64_t t_video;      /* T_v, a multiple of block (core.py:71-72) unless
+                           flags has RSA_SHAPE_RAGGED_VIDEO                    */
   int64_t t_text;       /* T_t >= 0                                          */
   int64_t head_dim;     /* d                                                 */
   int64_t block;        /* B: query and key block size                       */
   int32_t dtype;        /* rsa_dtype of Q/K/V/O                              */
   int32_t kernel;       /* rsa_kernel                                        */
+  int32_t flags;        /* RSA_SHAPE_* bits, 0 = the reference's rules        */
+  int32_t reserved;     /* 0                                                  */
 } rsa_shape;
 
 /* SparsityConfig (masks.py:21-41) + variant (rectify.py:23-24). */
@@ -79,6 +88,7 @@ typedef struct {
   int64_t n_text_blocks;
   int64_t last_text_block_len;
   int64_t n_cols;            /* N + T_t + n_text: columns of the score matrix */
+  int64_t last_video_block_len;  /* block, or T_v - (N-1)*block when ragged */
 } rsa_grid;
 
 /* Byte offsets of the intermediate results inside the workspace.  Every array

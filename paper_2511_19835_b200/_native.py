@@ -32,7 +32,10 @@ EXPORTS = ("rsa_plan", "rsa_workspace_layout_query", "rsa_workspace_size", "rsa_
 class Shape(C.Structure):
     _fields_ = [("heads", C.c_int64), ("t_video", C.c_int64), ("t_text", C.c_int64),
                 ("head_dim", C.c_int64), ("block", C.c_int64), ("dtype", C.c_int32),
-                ("kernel", C.c_int32)]
+                ("kernel", C.c_int32), ("flags", C.c_int32), ("reserved", C.c_int32)]
+
+
+SHAPE_RAGGED_VIDEO = 1   # rsa_shape.flags: final video block may hold < block tokens
 
 
 class Config(C.Structure):
@@ -43,7 +46,8 @@ class Config(C.Structure):
 
 class Grid(C.Structure):
     _fields_ = [("n_q", C.c_int64), ("n_kv", C.c_int64), ("n_text_blocks", C.c_int64),
-                ("last_text_block_len", C.c_int64), ("n_cols", C.c_int64)]
+                ("last_text_block_len", C.c_int64), ("n_cols", C.c_int64),
+                ("last_video_block_len", C.c_int64)]
 
 
 LAYOUT_FIELDS = ("q_pool", "q_def", "k_cat", "k_def", "v_pool", "scores", "a_pool", "mask_bits",
@@ -111,12 +115,13 @@ def check(status: int) -> None:
         raise STATUS_TO_ERROR.get(status, NativeError)(msg)
 
 
-def make_shape(heads, t_video, t_text, head_dim, block, dtype: str, kernel: str = "auto") -> Shape:
+def make_shape(heads, t_video, t_text, head_dim, block, dtype: str, kernel: str = "auto",
+               ragged_video: bool = False) -> Shape:
     if dtype not in DTYPE_CODES:
         from .errors import ShapeError
         raise ShapeError(f"q/k/v must be bfloat16, float32 or float64, got {dtype}")
     return Shape(int(heads), int(t_video), int(t_text), int(head_dim), int(block),
-                 DTYPE_CODES[dtype], KERNEL_CODES[kernel])
+                 DTYPE_CODES[dtype], KERNEL_CODES[kernel], SHAPE_RAGGED_VIDEO if ragged_video else 0, 0)
 
 
 def make_config(top_k_fraction, weight_threshold, adjacency_radius, force_text_blocks,

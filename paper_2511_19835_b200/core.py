@@ -69,6 +69,10 @@ class AttentionProblem:
     d: int
     block: int
     grid_dims: tuple | None = None
+    # extension: accept T_v % block != 0, the final
+    # video block holding the remaining T_v - (N-1)*block tokens; the reference
+    # raises BlockSizeError (core.py:71-72), which stays the default
+    ragged_video: bool = False
 
     def __post_init__(self):
         for name in ("q_video", "q_text", "k", "v"):
@@ -80,8 +84,10 @@ class AttentionProblem:
             raise ShapeError("k/v row counts must equal T_v + T_t")
         if self.block <= 0:
             raise BlockSizeError(f"block size must be positive, got {self.block}")
-        if self.t_v % self.block != 0:
+        if self.t_v % self.block != 0 and not self.ragged_video:
             raise BlockSizeError(f"T_v={self.t_v} is not divisible by block size {self.block}")
+        if self.t_v == 0:
+            raise ShapeError("T_v must be >= 1 block")
         kinds = {(_is_torch(m), dtype_name(m)) for m in (self.q_video, self.q_text, self.k, self.v)}
         if len(kinds) != 1:
             raise ShapeError(f"q/k/v dtypes disagree: {sorted(str(t) for t in kinds)}")
@@ -112,9 +118,22 @@ class BlockGrid:
     block: int
     text_block_start: int
     last_text_block_len: int
+    last_video_block_len: int | None = None   # None: block (ragged_video extension)
+
+    @property
+    def ragged(self) -> bool:
+        return self.last_video_block_len not in (None, self.block)
+
+    @property
+    def t_video(self) -> int:
+        return sum(self.q_block_lengths())
+
+    def q_block_lengths(self) -> list[int]:
+        last = self.block if self.last_video_block_len is None else self.last_video_block_len
+        return [self.block] * (self.n_q - 1) + [last]
 
     def kv_block_lengths(self) -> list[int]:
-        lens = [self.block] * self.n_q
+        lens = self.q_block_lengths()
         n_text = self.n_kv - self.n_q
         if n_text:
             lens += [self.block] * (n_text - 1) + [self.last_text_block_len]
@@ -138,13 +157,14 @@ def partition(problem: AttentionProblem) -> BlockGrid:
     b = problem.block
     if b <= 0:
         raise BlockSizeError(f"block size must be positive, got {b}")
-    if problem.t_v % b != 0:
+    if problem.t_v % b != 0 and not getattr(problem, "ragged_video", False):
         raise BlockSizeError(f"T_v={problem.t_v} is not divisible by block size {b}")
-    n_q = problem.t_v // b
+    n_q = -(-problem.t_v // b)
     n_text = -(-problem.t_t // b)
     last = problem.t_t - (n_text - 1) * b if n_text else 0
     return BlockGrid(n_q=n_q, n_kv=n_q + n_text, block=b, text_block_start=n_q,
-                     last_text_block_len=last)
+                     last_text_block_len=last,
+                     last_video_block_len=problem.t_v - (n_q - 1) * b if problem.t_v % b else None)
 
 
 @dataclass(frozen=True)
@@ -315,7 +335,7 @@ class PipelineResult:
 def stage_op_counts(grid: BlockGrid, d: int) -> dict:
     """Multiply-add counts of the pooled path per stage (rectify.py:179-193)."""
     n, m, b = grid.n_q, grid.n_kv, grid.block
-    t_v = n * b
+    t_v = grid.t_video
     t_t = grid.t_text
     t = t_v + t_t
     return {

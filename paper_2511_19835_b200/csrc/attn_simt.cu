@@ -75,7 +75,8 @@ attn_simt_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __re
     n = rem / subs;
     const int64_t sub = rem % subs;
     row0 = n * g.B + sub * QT;
-    nrows = min((int64_t)QT, g.B - sub * QT);
+    nrows = min((int64_t)QT, q_len(g, n) - sub * QT);
+    if (nrows <= 0) return;   // past the end of a ragged final video block (CTA-uniform)
   } else {
     const int64_t per_head = (g.qt_rows + QT - 1) / QT;
     h = blockIdx.x / per_head;
@@ -106,8 +107,8 @@ attn_simt_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __re
 
   for (int64_t it = 0; it < count; ++it) {
     const int64_t m = text ? it : list[it];
-    const int64_t kv0 = m * g.B;
-    const int64_t len = (m == g.M - 1 && g.n_text > 0) ? g.last_len : g.B;
+    const int64_t kv0 = kv_row0(g, m);
+    const int64_t len = kv_len(g, m);
     for (int64_t c0 = 0; c0 < len; c0 += KC) {
       const int64_t clen = min((int64_t)KC, len - c0);
       __syncthreads();

@@ -193,11 +193,11 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         const int panels = (is_v && VT) ? BKV / 64 : C::PANELS;
         for (int p = 0; p < panels; ++p)
           if (is_v && VT)   // V^T: box (64 keys, D dims) per 64-key panel
-            ptx::tma_load_3d_hint(dst + p * C::VT_PANEL, &tm_v, kv_full + s, (int)(m * g.B) + 64 * p, 0, (int)h, keep);
+            ptx::tma_load_3d_hint(dst + p * C::VT_PANEL, &tm_v, kv_full + s, (int)kv_row0(g, m) + 64 * p, 0, (int)h, keep);
           else if (is_v)    // V: box (64 dims, B keys) per 64-dim panel
-            ptx::tma_load_3d_hint(dst + p * C::KV_PANEL, &tm_v, kv_full + s, 64 * p, (int)(m * g.B), (int)h, keep);
+            ptx::tma_load_3d_hint(dst + p * C::KV_PANEL, &tm_v, kv_full + s, 64 * p, (int)kv_row0(g, m), (int)h, keep);
           else
-            ptx::tma_load_3d_hint(dst + p * C::KV_PANEL, &tm_k, kv_full + s, 64 * p, (int)(m * g.B), (int)h, keep);
+            ptx::tma_load_3d_hint(dst + p * C::KV_PANEL, &tm_k, kv_full + s, 64 * p, (int)kv_row0(g, m), (int)h, keep);
         ++it;
       };
       for (int64_t j = 0; j <= count; ++j) {
@@ -341,7 +341,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         m = m_first + j;
         member = true;
       }
-      const int len = (m == g.M - 1 && g.n_text > 0) ? (int)g.last_len : (int)g.B;
+      const int len = (int)kv_len(g, m);
       ptx::mbar_wait(s_full + (j % C::NS), (uint32_t)((j / C::NS) & 1));
       if (trace && sw == 0 && lane == 0 && j < 64) trace[j * 8 + 3] = clock64();
       ptx::tc_fence_after();
@@ -578,7 +578,7 @@ __device__ __forceinline__ void producer_loop(const CUtensorMap& tm_k, const CUt
 #pragma unroll
         for (int p = 0; p < C::PANELS; ++p)
           ptx::tma_load_3d_hint(dst + p * C::KV_PANEL, is_v ? &tm_v : &tm_k, kv_full + s, 64 * p,
-                                (int)(m * g.B), (int)t.h, keep);
+                                (int)kv_row0(g, m), (int)t.h, keep);
         if (++s == C::NST) { s = 0; ph ^= 1; }
       };
       for (int64_t j = 0; j <= t.count; ++j) {
@@ -764,7 +764,7 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid
           m = t.m_first + j;
           member = true;
         }
-        const int len = (m == g.M - 1 && g.n_text > 0) ? (int)g.last_len : (int)g.B;
+        const int len = (int)kv_len(g, m);
         ptx::mbar_wait(s_full + (gj % C::NS), (uint32_t)((gj / C::NS) & 1));
         if (tt && j == 0 && tix < 256) tt[tix * 4 + 0] = clock64();
         ptx::tc_fence_after();

@@ -41,7 +41,7 @@ rsa_status make_geometry(const rsa_shape* s, rsa::Geometry* g) {
   if (s->t_video < 0 || s->t_text < 0) return fail(RSA_ERR_SHAPE, "token counts must be >= 0");
   if (s->block <= 0)
     return fail(RSA_ERR_BLOCK_SIZE, "block size must be positive, got " + std::to_string(s->block));
-  if (s->t_video % s->block != 0)
+  if (s->t_video % s->block != 0 && !(s->flags & RSA_SHAPE_RAGGED_VIDEO))
     return fail(RSA_ERR_BLOCK_SIZE, "T_v=" + std::to_string(s->t_video) +
                                         " is not divisible by block size " + std::to_string(s->block));
   if (s->t_video == 0) return fail(RSA_ERR_SHAPE, "T_v must be >= 1 block");
@@ -51,7 +51,8 @@ rsa_status make_geometry(const rsa_shape* s, rsa::Geometry* g) {
   g->T = s->t_video + s->t_text;
   g->d = s->head_dim;
   g->B = s->block;
-  g->N = s->t_video / s->block;
+  g->N = (s->t_video + s->block - 1) / s->block;
+  g->q_last = s->t_video - (g->N - 1) * s->block;   // == B unless the final video block is ragged
   g->n_text = (s->t_text + s->block - 1) / s->block;
   g->M = g->N + g->n_text;
   g->last_len = g->n_text ? s->t_text - (g->n_text - 1) * s->block : 0;
@@ -193,6 +194,7 @@ rsa_status rsa_plan(const rsa_shape* shape, const rsa_config* cfg, rsa_grid* gri
     grid->n_text_blocks = g.n_text;
     grid->last_text_block_len = g.last_len;
     grid->n_cols = g.n_cols;
+    grid->last_video_block_len = g.q_last;
   }
   return RSA_OK;
 }
@@ -359,11 +361,11 @@ rsa_status rsa_text_full_attention(int64_t heads, int64_t n_queries, int64_t n_k
   if (n_keys < 1) return fail(RSA_ERR_SHAPE, "need at least one key row");
   // keys tiled by `block` from row 0 (kernel.py:138): full tiles as "video"
   // blocks, the remainder as one ragged trailing block
-  rsa_shape s{heads, (n_keys / block) * block, n_keys % block, head_dim, block, dtype, RSA_KERNEL_SIMT};
+  rsa_shape s{heads, (n_keys / block) * block, n_keys % block, head_dim, block, dtype, RSA_KERNEL_SIMT, 0, 0};
   rsa::Geometry g;
   g.H = heads; g.Tv = s.t_video; g.Tt = s.t_text; g.T = n_keys; g.d = head_dim; g.B = block;
   g.N = g.Tv / block; g.n_text = g.Tt > 0 ? 1 : 0; g.M = g.N + g.n_text;
-  g.last_len = g.Tt; g.n_cols = 0; g.dtype = dtype;
+  g.last_len = g.Tt; g.n_cols = 0; g.dtype = dtype; g.q_last = block;
   g.qt_rows = n_queries; g.qt_row0 = 0; g.q_rows = n_queries;
   if (dtype < RSA_BF16 || dtype > RSA_F64) return fail(RSA_ERR_SHAPE, "bad dtype");
   if (head_dim < 1 || head_dim > (dtype == RSA_F64 ? 128 : 256))
@@ -448,6 +450,7 @@ rsa_status rsa_diagnostics(const rsa_shape* shape, const void* q, const void* k,
   rsa::Geometry g;
   rsa_status s = make_geometry(shape, &g);
   if (s != RSA_OK) return s;
+  if (g.q_last != g.B) return fail(RSA_ERR_UNSUPPORTED, "diagnostics need full video blocks");
   if (!q || !k || !workspace || !gain || !error || !exact_gain || !exact_error || !s_sum || !s_sum_pool || !scratch)
     return fail(RSA_ERR_SHAPE, "null pointer");
   rsa::Workspace ws = bind(g, workspace);
@@ -469,6 +472,7 @@ rsa_status rsa_dense_reference(const rsa_shape* shape, const void* q, const void
   rsa::Geometry g;
   rsa_status s = make_geometry(shape, &g);
   if (s != RSA_OK) return s;
+  if (g.q_last != g.B) return fail(RSA_ERR_UNSUPPORTED, "diagnostics need full video blocks");
   if (!q || !k || !v || !out || !scratch) return fail(RSA_ERR_SHAPE, "null pointer");
   cudaError_t e = rsa::launch_dense_reference(g, q, k, v, out, scratch, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "dense_reference");

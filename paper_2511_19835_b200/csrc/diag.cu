@@ -50,9 +50,8 @@ __device__ double block_reduce_max(double x, double* red) {
   return red[0];
 }
 
-__device__ __forceinline__ double kv_len(const Geometry& g, int64_t m) {
-  return (m < g.N) ? (double)g.B : (m == g.M - 1 ? (double)g.last_len : (double)g.B);
-}
+// (the diagnostics reject a ragged final video block, capi.cu)
+__device__ __forceinline__ double kv_lenf(const Geometry& g, int64_t m) { return (double)kv_len(g, m); }
 // pooled score s_pool[n][m] (masks.py:120-127): video columns, then pooled text
 __device__ __forceinline__ double s_pool(const Geometry& g, const double* srow, int64_t m) {
   return m < g.N ? srow[m] : srow[g.N + g.Tt + (m - g.N)];
@@ -81,7 +80,7 @@ __global__ void __launch_bounds__(DT) diag_pooled_kernel(Workspace ws, Geometry 
   const bool deficit = ws.status[ST_DEFICIT] != 0;
   const int64_t d = g.d;
   for (int64_t m = threadIdx.x; m < M; m += DT) {
-    const double len = kv_len(g, m), s = s_pool(g, srow, m);
+    const double len = kv_lenf(g, m), s = s_pool(g, srow, m);
     const double at = exp(s - mx) / denom;
     a_tok[n * M + m] = at;
     exact_gain[(h * g.N + n) * M + m] = (double)g.B * len * at;
@@ -122,7 +121,7 @@ __global__ void __launch_bounds__(DT) diag_row_kernel(const double* __restrict__
   const double shift = fmax(mx, pmax[n]);
   const double* prow = ws.scores + (h * g.N + n) * g.n_cols;
   double pp = 0.0;
-  for (int64_t m = threadIdx.x; m < g.M; m += DT) pp += kv_len(g, m) * exp(s_pool(g, prow, m) - shift);
+  for (int64_t m = threadIdx.x; m < g.M; m += DT) pp += kv_lenf(g, m) * exp(s_pool(g, prow, m) - shift);
   const double pooled = block_reduce_sum(pp, red);
   if (threadIdx.x == 0) {
     rmax[r] = mx;
@@ -139,7 +138,7 @@ __global__ void __launch_bounds__(DT) diag_err_kernel(const double* __restrict__
                                                       const double* a_tok, double* exact_error, double sqrt_d) {
   __shared__ double red[DT / 32];
   const int64_t m = blockIdx.x, nl = blockIdx.y, n = n0 + nl;
-  const int64_t len = (int64_t)kv_len(g, m), start = m * g.B;
+  const int64_t len = kv_len(g, m), start = kv_row0(g, m);
   const double a = a_tok[n * g.M + m];
   double part = 0.0;
   for (int64_t idx = threadIdx.x; idx < g.B * len; idx += DT) {

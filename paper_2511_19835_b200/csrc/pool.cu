@@ -70,8 +70,8 @@ pool_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restric
   const int64_t nblocks = seg == 0 ? g.N : g.M;
   if (blk >= nblocks) return;
   const int64_t d = g.d;
-  const int64_t row0 = blk * g.B;  // text blocks follow the video blocks contiguously
-  const int64_t len = (blk < g.N) ? g.B : (blk == g.M - 1 ? g.last_len : g.B);
+  const int64_t row0 = kv_row0(g, blk);  // text blocks follow the video blocks contiguously
+  const int64_t len = kv_len(g, blk);
   const T* src = (seg == 0 ? q : seg == 1 ? k : v) + (h * g.T + row0) * d;
 
   __shared__ double s_hi[2048];
@@ -299,10 +299,10 @@ pool_bulk_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
   const int t = threadIdx.x;
   const int word = t % WPR, rp = t / WPR;
   auto src_of = [&](const PoolItem& it, uint32_t& bytes) -> const void* {
-    const int64_t len = (it.blk < g.N) ? g.B : (it.blk == g.M - 1 ? g.last_len : g.B);
+    const int64_t len = kv_len(g, it.blk);
     bytes = (uint32_t)(len * D * 2);
     const __nv_bfloat16* base = it.seg == 0 ? q : it.seg == 1 ? k : v;
-    return base + (it.h * g.T + it.blk * g.B) * D;
+    return base + (it.h * g.T + kv_row0(g, it.blk)) * D;
   };
   if (t == 0) {
     for (int s = 0; s < STAGES; ++s) bar_init(full + s, 1);
@@ -326,12 +326,12 @@ pool_bulk_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
   constexpr int CPR = D * 2 / 16;   // 16-byte pieces per row
   auto fetch_rows = [&](int64_t i, int s) {
     const PoolItem it = pool_item(g, i);
-    const int64_t len = (it.blk < g.N) ? g.B : (it.blk == g.M - 1 ? g.last_len : g.B);
+    const int64_t len = kv_len(g, it.blk);
     const __nv_bfloat16* base = (it.seg == 0 ? q : it.seg == 1 ? k : v) + it.h * g.T * D;
     uint8_t* dst = ring + s * stage_bytes;
     for (int64_t c = t; c < len * CPR; c += kBulkThreads) {
       const int64_t r = c / CPR, cc = c % CPR;
-      const int64_t row = it.blk < g.N ? perm[it.blk * g.B + r] : it.blk * g.B + r;
+      const int64_t row = it.blk < g.N ? perm[it.blk * g.B + r] : kv_row0(g, it.blk) + r;
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
                        (uint32_t)__cvta_generic_to_shared(dst + r * D * 2 + cc * 16)),
                    "l"(base + row * D + cc * 8)
@@ -355,7 +355,7 @@ pool_bulk_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
   for (int64_t i = blockIdx.x; i < n_items; i += gridDim.x, ++kk) {
     const int s = (int)(kk % STAGES);
     const PoolItem it = pool_item(g, i);
-    const int64_t len = (it.blk < g.N) ? g.B : (it.blk == g.M - 1 ? g.last_len : g.B);
+    const int64_t len = kv_len(g, it.blk);
     if (perm) {
       // this item's group (committed STAGES groups ago) has landed, all threads' pieces
       asm volatile("cp.async.wait_group %0;" ::"n"(STAGES - 1) : "memory");
@@ -367,7 +367,7 @@ pool_bulk_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
     if (kp && it.seg > 0 && t == 0) {
       if (perm) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> bulk read
       // the permuted K / V block, contiguous, for K3's TMA (shared -> global bulk copy)
-      __nv_bfloat16* dstp = (it.seg == 1 ? kp : vp) + (it.h * g.T + it.blk * g.B) * D;
+      __nv_bfloat16* dstp = (it.seg == 1 ? kp : vp) + (it.h * g.T + kv_row0(g, it.blk)) * D;
       asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n\t"
                    "cp.async.bulk.commit_group;" ::"l"(dstp),
                    "r"((uint32_t)__cvta_generic_to_shared(blk)), "r"((uint32_t)(len * D * 2))
@@ -381,7 +381,7 @@ pool_bulk_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
     // x -> x - 1; no carry crosses the halves)
     uint32_t pmax = 0, pmin = 0x7FFF7FFFu;
     const bool text_k = (it.seg == 1) && (it.blk >= g.N);
-    double* raw_out = text_k ? ws.k_cat + (it.h * g.n_cols + g.N + (it.blk * g.B - g.Tv)) * D : nullptr;
+    double* raw_out = text_k ? ws.k_cat + (it.h * g.n_cols + g.N + (kv_row0(g, it.blk) - g.Tv)) * D : nullptr;
 #pragma unroll 8
     for (int64_t r = rp; r < len; r += RP) {
       const uint32_t w = blk[r * WPR + word];

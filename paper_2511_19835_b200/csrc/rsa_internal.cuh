@@ -42,7 +42,24 @@ struct Geometry {
   // text-query layout (text_full_attention may have any query count):
   // text query i of head h is row qt_row0 + i of a [H][q_rows][d] buffer
   int64_t qt_rows, qt_row0, q_rows;
+  // token count of the last video block: B, or T_v - (N-1)B for a ragged final
+  // video block (opt-in extension; the reference
+  // raises BlockSizeError, core.py:71-72)
+  int64_t q_last;
 };
+
+// tokens in video (query) block n
+__host__ __device__ __forceinline__ int64_t q_len(const Geometry& g, int64_t n) {
+  return n == g.N - 1 ? g.q_last : g.B;
+}
+// tokens in kv block m: video blocks, then text blocks (only the last ragged)
+__host__ __device__ __forceinline__ int64_t kv_len(const Geometry& g, int64_t m) {
+  return m < g.N ? q_len(g, m) : (m == g.M - 1 ? g.last_len : g.B);
+}
+// first row of kv block m in [T] (text rows start at T_v)
+__host__ __device__ __forceinline__ int64_t kv_row0(const Geometry& g, int64_t m) {
+  return m < g.N ? m * g.B : g.Tv + (m - g.N) * g.B;
+}
 
 enum MaskBit : uint8_t {
   BIT_MASK = 1, BIT_IMPORTANCE = 2, BIT_COMP = 4, BIT_ADJ = 8, BIT_APPLIED = 16

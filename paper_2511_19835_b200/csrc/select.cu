@@ -162,14 +162,21 @@ __global__ void __launch_bounds__(RT) select_rows_kernel(SelectParams P) {
 
   // ---- reallocation (ipar.py:45-66) ----
   if (Tt > 0 && g.B > 1) {
+    // a ragged final video block stands for q_last tokens, not B:
+    // D = B * sum_{n<N-1} A_v + q_last * A_v[N-1] + sum A_t
+    const bool ragged = g.q_last != g.B;
     double pv = 0.0, pt = 0.0;
-    for (int64_t j = threadIdx.x; j < n_mix; j += RT) { if (j < N) pv += sa[j]; else pt += sa[j]; }
+    for (int64_t j = threadIdx.x; j < n_mix; j += RT) {
+      if (j < N) { if (!(ragged && j == N - 1)) pv += sa[j]; } else pt += sa[j];
+    }
     const double sum_v = block_sum(pv, red);
     const double sum_t = block_sum(pt, red);
-    const double D = (double)g.B * sum_v + sum_t;
+    const double D = ragged ? ((double)g.B * sum_v + (double)g.q_last * sa[N - 1]) + sum_t
+                            : (double)g.B * sum_v + sum_t;
     if (D <= 0.0) { if (threadIdx.x == 0) atomicOr(ws.status + ST_DEGENERATE, 1); }
+    __syncthreads();   // every thread has read sa[N - 1]
     for (int64_t j = threadIdx.x; j < n_mix; j += RT)
-      sa[j] = (j < N) ? ((double)g.B * sa[j]) / D : sa[j] / D;
+      sa[j] = (j < N) ? ((double)q_len(g, j) * sa[j]) / D : sa[j] / D;
     __syncthreads();
   }
   // ---- a_pool row: video part + text re-aggregation (ipar.py:76-83) ----
@@ -355,9 +362,10 @@ __global__ void __launch_bounds__(RT) select_rows_kernel(SelectParams P) {
   const bool deficit = ws.status[ST_DEFICIT] != 0;
   const int64_t d = g.d;
   for (int64_t m = threadIdx.x; m < M; m += RT) {
-    const double len = (m < N) ? (double)g.B : (m == M - 1 ? (double)g.last_len : (double)g.B);
+    const double len = (double)kv_len(g, m);
+    const double bq = (double)q_len(g, n);   // query block tokens (masks.py:146: B)
     const double s = (m < N) ? srow[m] : srow[N + Tt + (m - N)];
-    const double gain = fabs(((double)g.B * len) * s);
+    const double gain = fabs((bq * len) * s);
     double err = 0.0;
     if (deficit) {
       const int64_t krow = (m < N) ? m : N + Tt + (m - N);
@@ -368,7 +376,7 @@ __global__ void __launch_bounds__(RT) select_rows_kernel(SelectParams P) {
       double d1 = 0.0, d2 = 0.0;
       for (int64_t c = 0; c < d; ++c) { d1 = fma(qd[c], kp[c], d1); d2 = fma(qp[c], kd[c], d2); }
       const double t1 = (d1 * len) * P.inv_sqrt_d;
-      const double t2 = ((double)g.B * d2) * P.inv_sqrt_d;
+      const double t2 = (bq * d2) * P.inv_sqrt_d;
       err = fabs(t1 + t2);
     }
     uint8_t b = bits[m];
@@ -508,21 +516,30 @@ __global__ void __launch_bounds__(RT, sel_min_blocks(PER)) select_rows_reg_kerne
     if (t + i * RT < n_mix) v[i] = v[i] / tot;
   // ---- reallocation (ipar.py:45-66) ----
   if (Tt > 0 && B > 1) {
-    double pv = 0.0, pt = 0.0;
+    const int q_last = (int)P.g.q_last;
+    const bool ragged = q_last != B;   // see select_rows_kernel
+    double pv = 0.0, pt = 0.0, pl = 0.0;
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
       const int j = t + i * RT;
-      if (j < N) pv += v[i];
+      if (ragged && j == N - 1) pl = v[i];
+      else if (j < N) pv += v[i];
       else if (j < n_mix) pt += v[i];
     }
     const double sum_v = block_reduce(pv, red[2], add);
     const double sum_t = block_reduce(pt, red[3], add);
-    const double D = (double)B * sum_v + sum_t;
+    double D;
+    if (ragged) {
+      const double a_last = block_reduce(pl, red[5], add);   // one non-zero term: exact
+      D = ((double)B * sum_v + (double)q_last * a_last) + sum_t;
+    } else {
+      D = (double)B * sum_v + sum_t;
+    }
     if (D <= 0.0 && t == 0) atomicOr(P.ws.status + ST_DEGENERATE, 1);
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
       const int j = t + i * RT;
-      if (j < n_mix) v[i] = (j < N) ? ((double)B * v[i]) / D : v[i] / D;
+      if (j < n_mix) v[i] = (j < N) ? ((double)(j == N - 1 ? q_last : B) * v[i]) / D : v[i] / D;
     }
   }
 #pragma unroll
@@ -656,14 +673,15 @@ __global__ void __launch_bounds__(RT, sel_min_blocks(PER)) select_rows_reg_kerne
   // ---- GAPR gate (masks.py:138-186) ----
   const bool deficit = P.ws.status[ST_DEFICIT] != 0;
   const int d = (int)P.g.d;
+  const double bq = (double)q_len(P.g, n);   // query block tokens (masks.py:146: B)
   int kv_local = 0;
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
     const int m = m0 + i;
     if (m >= M) continue;
-    const double len = (m < N) ? (double)B : (m == M - 1 ? (double)P.g.last_len : (double)B);
+    const double len = (double)kv_len(P.g, m);
     const double s = (m < N) ? sc[m] : sc[N + Tt + (m - N)];
-    const double gain = fabs(((double)B * len) * s);
+    const double gain = fabs((bq * len) * s);
     double err = 0.0;
     if (deficit) {
       const int krow = (m < N) ? m : N + Tt + (m - N);
@@ -674,7 +692,7 @@ __global__ void __launch_bounds__(RT, sel_min_blocks(PER)) select_rows_reg_kerne
       double d1 = 0.0, d2 = 0.0;
       for (int c = 0; c < d; ++c) { d1 = fma(qd[c], kp[c], d1); d2 = fma(qp[c], kd[c], d2); }
       const double t1 = (d1 * len) * P.inv_sqrt_d;
-      const double t2 = ((double)B * d2) * P.inv_sqrt_d;
+      const double t2 = (bq * d2) * P.inv_sqrt_d;
       err = fabs(t1 + t2);
     }
     uint8_t bb = b[i];

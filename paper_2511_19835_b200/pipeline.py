@@ -83,7 +83,7 @@ def rectified_attention_pipeline(problem: AttentionProblem, config: SparsityConf
     k = _as_tensor(problem.k, dev).contiguous()
     v = _as_tensor(problem.v, dev).contiguous()
     dtype = str(q.dtype).replace("torch.", "")
-    shape = nat.make_shape(1, t_v, t_t, d, problem.block, dtype, kernel)
+    shape = nat.make_shape(1, t_v, t_t, d, problem.block, dtype, kernel, ragged_video=grid.ragged)
     cfg = nat.make_config(*_cfg_tuple(config), variant)
     nat.plan(shape, cfg)
     ws = workspace_for(shape, dev)
@@ -127,7 +127,8 @@ def _result(problem, grid: BlockGrid, shape, ws, out, lse, variant, acct, host) 
     mask = (bits & MASK_BIT) != 0
     conv = (lambda x: x.detach().cpu().numpy()) if host else (lambda x: x.clone())
     lens = torch.tensor(grid.kv_block_lengths(), dtype=torch.int64, device=bits.device)
-    acct.kernel_inner_product_ops = int((mask.to(torch.int64) * lens[None, :]).sum().item()) * grid.block * d
+    qlens = torch.tensor(grid.q_block_lengths(), dtype=torch.int64, device=bits.device)
+    acct.kernel_inner_product_ops = int((mask.to(torch.int64) * lens[None, :] * qlens[:, None]).sum().item()) * d
     acct.stage_ops = stage_op_counts(grid, d)
     out_dtype = problem.q_video.dtype
     o = conv(out)
@@ -167,8 +168,8 @@ def block_sparse_attention(q_v, k, v, mask, grid: BlockGrid, counters: dict | No
                     dev).to(torch.bool)
     if tuple(bm.shape) != (grid.n_q, grid.n_kv):
         raise ShapeError(f"mask shape {tuple(bm.shape)} != (N, M) = {(grid.n_q, grid.n_kv)}")
-    if q_v.shape[0] != grid.n_q * grid.block:
-        raise ShapeError(f"q_v has {q_v.shape[0]} rows, expected N*B = {grid.n_q * grid.block}")
+    if q_v.shape[0] != grid.t_video:
+        raise ShapeError(f"q_v has {q_v.shape[0]} rows, expected {grid.t_video} (the grid's video tokens)")
     if tuple(k.shape) != tuple(v.shape):
         raise ShapeError(f"k shape {tuple(k.shape)} != v shape {tuple(v.shape)}")
     empty = ~bm.any(dim=1)
@@ -180,7 +181,8 @@ def block_sparse_attention(q_v, k, v, mask, grid: BlockGrid, counters: dict | No
     q = torch.cat([qv, torch.zeros(t_t, d, dtype=qv.dtype, device=dev)]).contiguous()
     kk = _as_tensor(k, dev).contiguous()
     vv = _as_tensor(v, dev).contiguous()
-    shape = nat.make_shape(1, t_v, t_t, d, grid.block, str(q.dtype).replace("torch.", ""), kernel)
+    shape = nat.make_shape(1, t_v, t_t, d, grid.block, str(q.dtype).replace("torch.", ""), kernel,
+                           ragged_video=grid.ragged)
     ws = workspace_for(shape, dev)
     out = torch.zeros_like(q)
     lse = torch.empty(q.shape[0], dtype=torch.float32, device=dev)
@@ -190,7 +192,8 @@ def block_sparse_attention(q_v, k, v, mask, grid: BlockGrid, counters: dict | No
     nat.check(nat.lib().rsa_check_device_status(_ptr(ws), _stream()))
     if counters is not None:
         lens = torch.tensor(grid.kv_block_lengths(), dtype=torch.int64, device=dev)
-        ops = int((bm.to(torch.int64) * lens[None, :]).sum().item()) * grid.block * d
+        qlens = torch.tensor(grid.q_block_lengths(), dtype=torch.int64, device=dev)
+        ops = int((bm.to(torch.int64) * lens[None, :] * qlens[:, None]).sum().item()) * d
         counters["inner_product_ops"] = counters.get("inner_product_ops", 0) + ops
     o_video, ld = out[:t_v], lse[:t_v].to(torch.float64)
     if host:
@@ -238,7 +241,8 @@ def rectified_sparse_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor
                                kernel: str = "auto", lse: torch.Tensor | None = None,
                                workspace: torch.Tensor | None = None,
                                check_status: bool = False, heads_per_chunk: int = 1,
-                               grid_dims: tuple | None = None, morton: bool = False) -> torch.Tensor:
+                               grid_dims: tuple | None = None, morton: bool = False,
+                               ragged_video: bool = False) -> torch.Tensor:
     """Rectified block-sparse attention for every (batch, head) of q/k/v
     ([..., T, d], the last ``num_text_tokens`` rows text).  ``sparsity=s`` is
     shorthand for top_k_fraction = 1 - s with p = 0, r = 0, no forced text.
@@ -250,7 +254,10 @@ def rectified_sparse_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor
     the pipeline runs on the Morton-reordered problem, as the reference
     harness's ``morton_reorder`` option does (harness.py:172-173), with the
     gather fused into K1 and the scatter into the K3 epilogue -- inputs and
-    output stay in the original token order."""
+    output stay in the original token order.
+    ``ragged_video=True`` accepts a video token count that is not a multiple of
+    ``block`` (the final video block is shorter; an extension -- the reference
+    raises BlockSizeError), e.g. HunyuanVideo's exact 118,800 tokens."""
     if sparsity is not None:
         top_k_fraction, weight_threshold, adjacency_radius, force_text_blocks = 1.0 - sparsity, 0.0, 0, False
     if top_k_fraction is None:
@@ -261,7 +268,8 @@ def rectified_sparse_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor
     T, d = q.shape[-2], q.shape[-1]
     heads = int(np.prod(q.shape[:-2]))
     t_t = int(num_text_tokens)
-    shape = nat.make_shape(heads, T - t_t, t_t, d, block, str(q.dtype).replace("torch.", ""), kernel)
+    shape = nat.make_shape(heads, T - t_t, t_t, d, block, str(q.dtype).replace("torch.", ""), kernel,
+                           ragged_video=ragged_video)
     cfg = nat.make_config(top_k_fraction, weight_threshold, adjacency_radius, force_text_blocks, variant)
     nat.plan(shape, cfg)
     if not q.is_cuda:
