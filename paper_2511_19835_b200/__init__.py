@@ -23,6 +23,8 @@ _LAZY = {"rectified_attention_pipeline", "block_sparse_attention", "text_full_at
 _REORDER = {"morton_permutation", "reorder_morton", "inverse_permutation"}
 _DIAG = {"gain_error", "gapr_condition_agreement", "denominator_equivalence_report"}
 _HARNESS = {"run_variants", "full_attention_reference", "normalized_l1", "cosine_similarity", "AlignmentReport"}
+_EXPERIMENT = {"SyntheticSpec", "ExperimentConfig", "gen_synthetic", "load_problem", "save_problem",
+               "run_experiment", "sweep_sparsity"}
 
 
 def __getattr__(name):
@@ -39,4 +41,7 @@ def __getattr__(name):
     if name in _HARNESS:
         from . import harness
         return getattr(harness, name)
+    if name in _EXPERIMENT:
+        from . import experiment
+        return getattr(experiment, name)
     raise AttributeError(name)
