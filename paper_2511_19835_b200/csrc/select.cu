@@ -24,6 +24,7 @@
 
 #include <cublas_v2.h>
 
+#include <algorithm>
 #include <cfloat>
 #include <cstdlib>
 
@@ -131,10 +132,13 @@ __global__ void __launch_bounds__(RT) select_rows_kernel(SelectParams P) {
   const int64_t n = blockIdx.x, h = blockIdx.y;
   const int64_t N = g.N, M = g.M, Tt = g.Tt, n_cols = g.n_cols;
   const int64_t n_mix = N + Tt;
+  // sa is dead once the a_pool row is built, so the sort values alias it
+  // (keeps M = 8192 kv blocks with p > 0 inside 227 KB of shared memory)
+  const int64_t sa_len = n_mix > P.p2 ? n_mix : P.p2;
   double* sa = reinterpret_cast<double*>(smem_raw);     // [n_mix] a_mix / a_hat
-  double* ap = sa + n_mix;                               // [M] a_pool row
-  double* sv = ap + M;                                   // [p2] sort values
-  int* si = reinterpret_cast<int*>(sv + P.p2);           // [p2] sort indices
+  double* sv = sa;                                       // [p2] sort values (after a_pool)
+  double* ap = sa + sa_len;                              // [M] a_pool row
+  int* si = reinterpret_cast<int*>(ap + M);              // [p2] sort indices
   uint8_t* bits = reinterpret_cast<uint8_t*>(si + P.p2); // [M]
   __shared__ double red[RT / 32];
   __shared__ int scan_tmp[RT];
@@ -847,7 +851,8 @@ cudaError_t launch_select(const Geometry& g, const rsa_config& cfg, int64_t k_fl
                   : launch(select_rows_reg_kernel<16>);
     if (e != cudaSuccess) return e;
   } else {
-    const size_t smem = (size_t)(g.N + g.Tt) * 8 + (size_t)g.M * 8 + (size_t)p2 * 12 + (size_t)g.M + 16;
+    const size_t sa_len = std::max<size_t>((size_t)(g.N + g.Tt), (size_t)p2);
+    const size_t smem = sa_len * 8 + (size_t)g.M * 8 + (size_t)p2 * 4 + (size_t)g.M + 16;
     if (smem > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(select_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;

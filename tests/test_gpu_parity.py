@@ -391,3 +391,30 @@ def test_select_rows_wide_rows_vs_oracle(block, n_q, t_t, f, p, radius, force):
     np.testing.assert_array_equal(res.comp_mask.mask, comp)
     np.testing.assert_allclose(res.implicit.a_pool, imp["a_pool"], atol=1e-12, rtol=0)
     np.testing.assert_allclose(res.factors.r, O.rect_factors(imp["a_pool"], sel["mask"]), atol=1e-12, rtol=0)
+
+
+@pytest.mark.parametrize("p", [0.0, 0.5])
+def test_select_rows_max_kv_blocks(p):
+    """The C ABI's upper bound, M = 8192 kv blocks (T_v = 65,536 at B = 8): the
+    general row kernel's shared memory fits with the cumulative-weight sort
+    (p > 0) too; a sample of rows bit-exact against the oracle (rows are
+    independent in a3-a7, so the oracle runs on the sampled q_pool rows only)."""
+    block, d, n_q = 8, 8, 8192
+    qv, qt, k, v = O.random_problem(9, t_v=block * n_q, t_t=0, d=d, dtype=np.float32)
+    res = run_np(qv, qt, k, v, block, 0.1, p, 0, False, "sparse-rectified")
+    rows = np.linspace(0, n_q - 1, 48).astype(int)
+    pooled = O.pool(qv, k, v, 0, block)
+    # T_t = 0: a_pool = the mixed softmax itself (ipar.py:59-60 identity bypass)
+    a_pool = O.softmax_rows((pooled["q_pool"][rows] @ pooled["k_mix"].T) / np.sqrt(d))
+    sel = O.select_mask(a_pool, 0.1, p, 0, False, n_q)
+    # (select_mask's adjacency band indexes the sampled rows 0..47: compare the
+    # importance set and add the diagonal (radius 0) at the true row indices)
+    np.testing.assert_array_equal(res.sparse_mask.importance[rows], sel["importance"])
+    want = sel["importance"].copy()
+    want[np.arange(rows.size), rows] = True
+    np.testing.assert_array_equal(res.sparse_mask.mask[rows], want)
+    np.testing.assert_allclose(res.implicit.a_pool[rows], a_pool, atol=1e-12, rtol=0)
+    with pytest.raises(rsa.NativeError):
+        # one block more than the bound
+        run_np(np.concatenate([qv, qv[:8]]), qt, np.concatenate([k, k[:8]]), np.concatenate([v, v[:8]]),
+               block, 0.1, p, 0, False, "sparse-rectified")
