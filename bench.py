@@ -64,6 +64,8 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="hv")
     ap.add_argument("--sparsity", type=float, default=0.9)
+    ap.add_argument("--weight-threshold", type=float, default=0.0,
+                    help="cumulative-weight rule p (masks.py:99-103); the headline config uses 0")
     ap.add_argument("--variant", default="sparse-rectified")
     ap.add_argument("--kernel", default="auto", choices=["auto", "tcgen05", "simt"])
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -320,7 +322,7 @@ def run_ours(args):
     T, d = q.shape[1], q.shape[2]
     shape = nat.make_shape(heads, cfg["t_v"], cfg["t_t"], d, cfg["block"], "bfloat16", args.kernel,
                            ragged_video=cfg.get("ragged", False))
-    conf = nat.make_config(f, 0.0, 0, False, args.variant)
+    conf = nat.make_config(f, args.weight_threshold, 0, False, args.variant)
     grid = nat.plan(shape, conf)
     ws = workspace_for(shape, dev)
     out = torch.empty_like(q)
@@ -357,7 +359,8 @@ def run_ours(args):
 
         def uattn(q_, k_, v_, t_t_):
             return rsa.rectified_sparse_attention(q_, k_, v_, num_text_tokens=t_t_, block=cfg["block"],
-                                                  top_k_fraction=f, variant=args.variant, kernel=args.kernel,
+                                                  top_k_fraction=f, weight_threshold=args.weight_threshold,
+                                                  variant=args.variant, kernel=args.kernel,
                                                   workspace=ws)
 
         def step(record=False):
@@ -437,7 +440,7 @@ def run_ours(args):
             # the public call on HOST tensors: H2D of q/k/v, K1 -> K2 -> K3 and the
             # D2H of the output, pipelined over chunks of heads (rsa_forward_host)
             out_box[:] = [rsa.rectified_sparse_attention(hq[None], hk[None], hv[None], num_text_tokens=cfg["t_t"],
-                                                         block=cfg["block"], top_k_fraction=f,
+                                                         block=cfg["block"], top_k_fraction=f, weight_threshold=args.weight_threshold,
                                                          variant=args.variant, kernel=args.kernel,
                                                          workspace=ws, heads_per_chunk=args.e2e_chunk,
                                                          ragged_video=cfg.get("ragged", False))]
@@ -488,7 +491,7 @@ def run_ours(args):
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (gen_synthetic-style, torch RNG)",
         "config": {"workload": cfg["label"], "heads": cfg["heads"], "t_video": cfg["t_v"], "t_text": cfg["t_t"],
                    "head_dim": d, "block": cfg["block"], "top_k_fraction": round(f, 6),
-                   "weight_threshold": 0.0, "adjacency_radius": 0, "force_text_blocks": False,
+                   "weight_threshold": args.weight_threshold, "adjacency_radius": 0, "force_text_blocks": False,
                    "variant": args.variant,
                    "parallelism": (f"Ulysses seq->head all-to-all x{world} (NCCL)" if ulysses
                                    else f"head-sharded x{world}"),

@@ -125,6 +125,30 @@ __device__ void bitonic_sort(double* sv, int* si, int n) {
   }
 }
 
+// Sequential cumsum of v[0..n) in order, exactly numpy.cumsum's rounding
+// (masks.py:99): the first k with v[0] + ... + v[k-1] >= p, or 0 if none.
+// One thread; loads batched ahead of the dependent adds (shared-memory latency
+// would otherwise serialise with every add).
+__device__ int seq_first_reach(const double* v, int n, double p) {
+  double cum = 0.0;
+  int j = 0;
+  for (; j + 8 <= n; j += 8) {
+    double x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = v[j + u];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      cum += x[u];
+      if (cum >= p) return j + u + 1;
+    }
+  }
+  for (; j < n; ++j) {
+    cum += v[j];
+    if (cum >= p) return j + 1;
+  }
+  return 0;
+}
+
 __global__ void __launch_bounds__(RT) select_rows_kernel(SelectParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Geometry& g = P.g;
@@ -314,11 +338,7 @@ __global__ void __launch_bounds__(RT) select_rows_kernel(SelectParams P) {
       for (int i = tot_k + threadIdx.x; i < kp2; i += RT) { sv[i] = -1.0; si[i] = 0x7fffffff; }
       __syncthreads();
       bitonic_sort(sv, si, kp2);
-      if (threadIdx.x == 0) {
-        double cum = 0.0;
-        for (int64_t i = 0; i < K; ++i) cum += sv[i];
-        sh_count = cum >= P.p ? 0 : 1;
-      }
+      if (threadIdx.x == 0) sh_count = seq_first_reach(sv, (int)K, P.p) ? 0 : 1;
       __syncthreads();
       need_full_sort = sh_count != 0;
     }
@@ -333,12 +353,8 @@ __global__ void __launch_bounds__(RT) select_rows_kernel(SelectParams P) {
       bitonic_sort(sv, si, P.p2);
       if (threadIdx.x == 0) {
         // sequential cumsum in sorted order, exactly as numpy.cumsum (masks.py:99-102)
-        int64_t first_p = M;
-        double cum = 0.0;
-        for (int64_t i = 0; i < M; ++i) {
-          cum += sv[i];
-          if (cum >= P.p) { first_p = i + 1; break; }
-        }
+        const int reach = seq_first_reach(sv, (int)M, P.p);
+        const int64_t first_p = reach ? reach : M;
         int64_t count = first_p > P.k_floor ? first_p : P.k_floor;
         count = count < 1 ? 1 : (count > M ? M : count);
         sh_count = (int)count;
@@ -469,7 +485,11 @@ __device__ __forceinline__ int block_scan(int x, int* slot, int* total) {
 // 1.07 vs 1.46 ms for the whole K2 at HunyuanVideo size with the compiler's 96 registers)
 constexpr int sel_min_blocks(int per) { return per <= 10 ? 8 : per <= 12 ? 6 : 4; }
 
-template <int PER>
+// CUM: the cumulative-weight rule is on (p > 0).  The top-K found by the radix
+// select already satisfies it when its sum clears p by more than any summation
+// order can move it (K * eps relative); otherwise the row is sorted in shared
+// memory and the sequential cumsum decides the count exactly (masks.py:99-103).
+template <int PER, bool CUM>
 __global__ void __launch_bounds__(RT, sel_min_blocks(PER)) select_rows_reg_kernel(SelectParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int N = (int)P.g.N, M = (int)P.g.M, Tt = (int)P.g.Tt, n_cols = (int)P.g.n_cols;
@@ -482,7 +502,12 @@ __global__ void __launch_bounds__(RT, sel_min_blocks(PER)) select_rows_reg_kerne
   double* sa = sc + n_cols;                            // [n_mix] a_hat
   double* at = sa + n_mix;                             // [n_text] text a_pool columns
   uint8_t* sb = reinterpret_cast<uint8_t*>(at + n_text);  // [M] mask bits
-  __shared__ double red[6][NW];
+  // CUM only: [p2] sort values, [p2] sort indices, [M] importance flags
+  double* sv = reinterpret_cast<double*>(((uintptr_t)(sb + M) + 15) & ~(uintptr_t)15);
+  int* si = reinterpret_cast<int*>(sv + P.p2);
+  uint8_t* simp = reinterpret_cast<uint8_t*>(si + P.p2);
+  __shared__ double red[7][NW];
+  __shared__ int sh_count;
   __shared__ int ired[2][NW];
   __shared__ unsigned hist[2][256];
   __shared__ unsigned long long s_and[NW], s_or[NW];
@@ -654,13 +679,46 @@ __global__ void __launch_bounds__(RT, sel_min_blocks(PER)) select_rows_reg_kerne
       eq += (m0 + i < M && ((uint64_t)__double_as_longlong(a[i]) & pmask) == prefix) ? 1 : 0;
     int tot_eq;
     int rank = block_scan(eq, ired[0], &tot_eq);
+    bool sel[PER];
+    double top_sum = 0.0;
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
       const int m = m0 + i;
       const uint64_t key = (uint64_t)__double_as_longlong(a[i]) & pmask;
-      bool sel = false;
-      if (m < M) sel = key > prefix || (key == prefix && rank++ < remaining);
-      uint8_t bb = sel ? BIT_IMPORTANCE : 0;
+      sel[i] = false;
+      if (m < M) sel[i] = key > prefix || (key == prefix && rank++ < remaining);
+      top_sum += sel[i] ? a[i] : 0.0;
+    }
+    if (CUM) {
+      const double S = block_reduce(top_sum, red[6], [](double x, double y) { return x + y; });
+      if (!(S - 4.0 * (double)K * DBL_EPSILON * S >= P.p)) {
+        // p may bind: sort the whole row (value desc, index asc) and take the
+        // sequential cumsum, as the general kernel does
+        for (int j = t; j < P.p2; j += RT) {
+          const int src = j;
+          sv[j] = src < M ? (src < N ? sa[src] : at[src - N]) : -1.0;
+          si[j] = src < M ? src : 0x7fffffff;
+        }
+        for (int j = t; j < M; j += RT) simp[j] = 0;
+        __syncthreads();
+        bitonic_sort(sv, si, P.p2);
+        if (t == 0) {
+          const int reach = seq_first_reach(sv, M, P.p);
+          const int first_p = reach ? reach : M;
+          int count = first_p > K ? first_p : K;
+          sh_count = count < 1 ? 1 : (count > M ? M : count);
+        }
+        __syncthreads();
+        for (int j = t; j < sh_count; j += RT) simp[si[j]] = 1;
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < PER; ++i) sel[i] = m0 + i < M && simp[m0 + i];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int m = m0 + i;
+      uint8_t bb = sel[i] ? BIT_IMPORTANCE : 0;
       const int dist = m > n ? m - n : n - m;
       if (dist <= P.radius) bb |= BIT_ADJ;
       if ((bb & (BIT_IMPORTANCE | BIT_ADJ)) || (P.force_text && M > N && m >= N)) bb |= BIT_MASK;
@@ -832,9 +890,11 @@ cudaError_t launch_select(const Geometry& g, const rsa_config& cfg, int64_t k_fl
   // the general one (A/B)
   static const int reg_env = [] { const char* e = getenv("RSA_SELECT_REG"); return e ? atoi(e) : 1; }();
   const int per = (int)((g.n_cols + RT - 1) / RT);
-  const bool reg = reg_env != 0 && !(P.p > 0.0) && !P.use_sort && per <= 16;
+  const bool cum = P.p > 0.0;
+  const bool reg = reg_env != 0 && !P.use_sort && per <= 16;
   if (reg) {
-    const size_t smem = (size_t)(g.n_cols + g.N + g.Tt + g.n_text) * 8 + (size_t)g.M + 16;
+    size_t smem = (size_t)(g.n_cols + g.N + g.Tt + g.n_text) * 8 + (size_t)g.M + 16;
+    if (cum) smem += 16 + (size_t)p2 * 12 + (size_t)g.M;
     auto launch = [&](auto kern) -> cudaError_t {
       if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -843,12 +903,20 @@ cudaError_t launch_select(const Geometry& g, const rsa_config& cfg, int64_t k_fl
       kern<<<dim3((unsigned)g.N, (unsigned)g.H), RT, smem, st>>>(P);
       return cudaSuccess;
     };
-    cudaError_t e = per <= 4 ? launch(select_rows_reg_kernel<4>)
-                  : per <= 6 ? launch(select_rows_reg_kernel<6>)
-                  : per <= 8 ? launch(select_rows_reg_kernel<8>)
-                  : per <= 10 ? launch(select_rows_reg_kernel<10>)
-                  : per <= 12 ? launch(select_rows_reg_kernel<12>)
-                  : launch(select_rows_reg_kernel<16>);
+    cudaError_t e;
+    if (cum)
+      e = per <= 4 ? launch(select_rows_reg_kernel<4, true>)
+        : per <= 8 ? launch(select_rows_reg_kernel<8, true>)
+        : per <= 10 ? launch(select_rows_reg_kernel<10, true>)
+        : per <= 12 ? launch(select_rows_reg_kernel<12, true>)
+        : launch(select_rows_reg_kernel<16, true>);
+    else
+      e = per <= 4 ? launch(select_rows_reg_kernel<4, false>)
+        : per <= 6 ? launch(select_rows_reg_kernel<6, false>)
+        : per <= 8 ? launch(select_rows_reg_kernel<8, false>)
+        : per <= 10 ? launch(select_rows_reg_kernel<10, false>)
+        : per <= 12 ? launch(select_rows_reg_kernel<12, false>)
+        : launch(select_rows_reg_kernel<16, false>);
     if (e != cudaSuccess) return e;
   } else {
     const size_t sa_len = std::max<size_t>((size_t)(g.N + g.Tt), (size_t)p2);
