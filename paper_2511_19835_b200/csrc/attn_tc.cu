@@ -79,6 +79,7 @@ struct TcParams {
   float scale_log2;  // log2(e) / sqrt(d)
   int trace_cta;     // CTA traced per step when stamps == 2
   int stamps;        // RSA_TC_STAMPS=1: per-CTA globaltimer stamps into `lse` (profiling)
+  int qring;         // persistent kernel: each tile's Q rows arrive by TMA in a K/V ring stage
   int mode;          // 0 normal; diagnostics: 1 no softmax math, 2 TMA only, 3 MMA only, 4 MMA+TMA,
                      // 6 softmax only, 7 normal + per-CTA globaltimer stamps into `lse`
 };
@@ -554,22 +555,35 @@ __device__ __forceinline__ TileDesc decode_tile(const TcParams& P, int64_t bid) 
 }
 
 template <int D, int BKV>
-__device__ __forceinline__ void producer_loop(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const TcParams& P,
+__device__ __forceinline__ void producer_loop(const CUtensorMap& tm_q, const CUtensorMap& tm_k, const CUtensorMap& tm_v, const TcParams& P,
                                    int64_t n_tiles, uint8_t* kv_s, uint64_t* q_full, uint64_t* kv_full,
                                    uint64_t* kv_empty, uint64_t* s_full, uint64_t* p_full, uint64_t* pv_done,
                                    uint32_t tmem, int lane) {
   using C = Cfg<D, BKV, true, false>;
   const Geometry& g = P.g;
   (void)g; (void)q_full; (void)s_full; (void)p_full; (void)pv_done; (void)tmem; (void)tm_v;
-  // ===================== TMA producer: every tile's K_0 K_1 V_0 K_2 V_1 ... =====================
+  // ===================== TMA producer: every tile's [Q] K_0 K_1 V_0 K_2 V_1 ... =====================
   if (lane == 0) {
+    if (P.qring) ptx::prefetch_tmap(&tm_q);
     ptx::prefetch_tmap(&tm_k);
     ptx::prefetch_tmap(&tm_v);
     const uint64_t keep = ptx::policy_evict_last();   // K/V blocks are re-read by many tiles of the head
+    const uint64_t once = ptx::policy_evict_first();  // Q rows are read by one tile
     int s = 0;
     uint32_t ph = 0;
     for (int64_t bid = blockIdx.x; bid < n_tiles; bid += gridDim.x) {
       const TileDesc t = decode_tile(P, bid);
+      if (P.qring) {
+        // the tile's Q rows take one ring stage ahead of its K/V, so they are
+        // in shared memory long before the softmax warps move them into TMEM
+        ptx::mbar_wait(kv_empty + s, ph ^ 1);
+        ptx::mbar_expect_tx(kv_full + s, C::STAGE);
+        uint8_t* dst = kv_s + s * C::STAGE;
+#pragma unroll
+        for (int p = 0; p < C::PANELS; ++p)
+          ptx::tma_load_3d_hint(dst + p * C::Q_PANEL, &tm_q, kv_full + s, 64 * p, (int)t.q_row0, (int)t.h, once);
+        if (++s == C::NST) { s = 0; ph ^= 1; }
+      }
       auto load = [&](int64_t j, bool is_v) {
         const int64_t m = t.list ? (t.list[j] & 0xFFFFFF) : t.m_first + j;
         ptx::mbar_wait(kv_empty + s, ph ^ 1);
@@ -612,6 +626,12 @@ __device__ __forceinline__ void mma_loop(const CUtensorMap& tm_k, const CUtensor
     ptx::mbar_wait(q_full, tile_par);   // this tile's Q rows are in TMEM
     tile_par ^= 1u;
     ptx::tc_fence_after();
+    if (P.qring) {
+      // every softmax thread has copied its Q row out of the ring stage: free it
+      if (lane == 0) ptx::mbar_arrive(kv_empty + s_kv);
+      __syncwarp();
+      advance();
+    }
     for (int64_t j = 0; j <= count; ++j) {
       if (j < count) {
         const int64_t gj = gs + j;
@@ -657,8 +677,8 @@ __device__ __forceinline__ void mma_loop(const CUtensorMap& tm_k, const CUtensor
 
 template <int D, int BKV, int WPQ, int EMU>
 __global__ void __launch_bounds__(128 + 128 * WPQ, 1)
-attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
-                          const TcParams P, int64_t n_tiles) {
+attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                          const __grid_constant__ CUtensorMap tm_v, const TcParams P, int64_t n_tiles) {
   using C = Cfg<D, BKV, true, false>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -696,7 +716,7 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    producer_loop<D, BKV>(tm_k, tm_v, P, n_tiles, kv_s, q_full, kv_full, kv_empty, s_full, p_full, pv_done, tmem, lane);
+    producer_loop<D, BKV>(tm_q, tm_k, tm_v, P, n_tiles, kv_s, q_full, kv_full, kv_empty, s_full, p_full, pv_done, tmem, lane);
   } else if (warp == 1) {
     mma_loop<D, BKV>(tm_k, tm_v, P, n_tiles, kv_s, q_full, kv_full, kv_empty, s_full, p_full, pv_done, tmem, lane);
   } else if (warp >= 4) {
@@ -717,16 +737,34 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid
     const uint64_t once = ptx::policy_evict_first();   // Q rows and outputs are touched once
     // Q row -> TMEM lanes (A operand of S = Q K^T): this thread packs half of
     // its row's d columns, bf16 pairs per 32-bit column
+    int64_t ring_pos = 0;   // K/V ring stages consumed before the current tile (qring)
     auto store_q = [&](const TileDesc& t) {
       uint32_t qw[QW];
-      const int64_t grow = t.q_row0 + row;
-      // permuted problem: gather the query row from its original position
-      const int64_t srow = (P.perm && grow < g.Tv) ? P.perm[grow] : grow;
-      const uint4* src = reinterpret_cast<const uint4*>(P.q + (t.h * g.T + srow) * D + half * (D / WPQ));
+      if (P.qring) {
+        // this thread's D / WPQ columns of its row from the tile's Q ring stage
+        // (TMA 128B-swizzled panels of 64 columns: 16-byte chunk c of row r at
+        // chunk slot c ^ (r % 8))
+        const int st = (int)(ring_pos % C::NST);
+        ptx::mbar_wait(kv_full + st, (uint32_t)((ring_pos / C::NST) & 1));
+        const uint8_t* stage = kv_s + st * C::STAGE;
 #pragma unroll
-      for (int i = 0; i < QW / 4; ++i) {
-        const uint4 x = grow < g.T ? ptx::ld_stream(src + i, once) : make_uint4(0, 0, 0, 0);
-        qw[4 * i] = x.x; qw[4 * i + 1] = x.y; qw[4 * i + 2] = x.z; qw[4 * i + 3] = x.w;
+        for (int i = 0; i < QW / 4; ++i) {
+          const int col16 = half * (QW / 4) + i;             // 16-byte chunk of the row (8 per panel)
+          const uint8_t* pan = stage + (col16 / 8) * C::Q_PANEL + row * 128;
+          const uint4 x = *reinterpret_cast<const uint4*>(pan + (((col16 % 8) ^ (row % 8)) * 16));
+          qw[4 * i] = x.x; qw[4 * i + 1] = x.y; qw[4 * i + 2] = x.z; qw[4 * i + 3] = x.w;
+        }
+        ring_pos += 1 + 2 * t.count;
+      } else {
+        const int64_t grow = t.q_row0 + row;
+        // permuted problem: gather the query row from its original position
+        const int64_t srow = (P.perm && grow < g.Tv) ? P.perm[grow] : grow;
+        const uint4* src = reinterpret_cast<const uint4*>(P.q + (t.h * g.T + srow) * D + half * (D / WPQ));
+#pragma unroll
+        for (int i = 0; i < QW / 4; ++i) {
+          const uint4 x = grow < g.T ? ptx::ld_stream(src + i, once) : make_uint4(0, 0, 0, 0);
+          qw[4 * i] = x.x; qw[4 * i + 1] = x.y; qw[4 * i + 2] = x.z; qw[4 * i + 3] = x.w;
+        }
       }
       if constexpr (QW == 32) {
         ptx::tmem_st32(lane_base + C::Q_COL + half * QW, qw);
@@ -1040,10 +1078,15 @@ cudaError_t launch_persistent(const Geometry& g, const void* q, const void* k, c
                               float* lse, const Workspace& ws, bool rectify, bool text, cudaStream_t st,
                               const int32_t* perm) {
   using C = Cfg<D, BKV, true, false>;
-  CUtensorMap tk, tv;
-  if (!make_tmap_3d(&tk, k, g.d, g.T, g.H, BKV) || !make_tmap_3d(&tv, v, g.d, g.T, g.H, BKV))
+  CUtensorMap tq, tk, tv;
+  if (!make_tmap_3d(&tq, q, g.d, g.T, g.H, 128) || !make_tmap_3d(&tk, k, g.d, g.T, g.H, BKV) ||
+      !make_tmap_3d(&tv, v, g.d, g.T, g.H, BKV))
     return cudaErrorInvalidValue;
   TcParams P{};
+  // Q through the ring when a Q tile is exactly one stage (BKV = 128) and rows
+  // are not gathered through a permutation; RSA_TC_QRING=0 loads Q rows directly
+  static const int qring_env = [] { const char* e = getenv("RSA_TC_QRING"); return e ? atoi(e) : 1; }();
+  P.qring = (qring_env != 0 && C::STAGE == C::Q_BYTES && perm == nullptr) ? 1 : 0;
   P.g = g;
   P.ws = ws;
   P.out = static_cast<__nv_bfloat16*>(out);
@@ -1071,7 +1114,7 @@ cudaError_t launch_persistent(const Geometry& g, const void* q, const void* k, c
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t n_tiles = g.H * P.tiles_per_head;
-  kern<<<(unsigned)std::min<int64_t>(n_tiles, sms), 128 + 128 * WPQ, smem, st>>>(tk, tv, P, n_tiles);
+  kern<<<(unsigned)std::min<int64_t>(n_tiles, sms), 128 + 128 * WPQ, smem, st>>>(tq, tk, tv, P, n_tiles);
   e = cudaGetLastError();
   if (e != cudaSuccess || P.text_tiles_per_head == 0) return e;
   text_combine_kernel<D><<<(unsigned)(g.H * P.text_tiles_per_head), 256, 0, st>>>(
