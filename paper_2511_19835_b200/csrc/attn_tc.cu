@@ -145,8 +145,13 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     const int64_t t = r_in - n_text_ct;
     q_row0 = t * 128;
     rows_valid = min((int64_t)128, g.Tv - q_row0);
-    count = P.ws.tile_count[h * P.video_tiles_per_head + t];
-    list = P.ws.tile_list + (h * P.video_tiles_per_head + t) * g.M;
+    if (g.B == 128) {   // one query block per tile: its own kv list (tile_lists skipped)
+      count = P.ws.kv_count[h * g.N + t];
+      list = P.ws.kv_list + (h * g.N + t) * g.M;
+    } else {
+      count = P.ws.tile_count[h * P.video_tiles_per_head + t];
+      list = P.ws.tile_list + (h * P.video_tiles_per_head + t) * g.M;
+    }
   }
 
   if (threadIdx.x == 0) {
@@ -337,7 +342,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       if (list) {
         const int32_t e = list[j];
         m = e & 0xFFFFFF;
-        member = (e >> (24 + sub)) & 1;
+        member = BKV == 128 || ((e >> (24 + sub)) & 1);   // plain kv-list entries at B = 128
       } else {
         m = m_first + j;
         member = true;
@@ -548,8 +553,13 @@ __device__ __forceinline__ TileDesc decode_tile(const TcParams& P, int64_t bid) 
     const int64_t tt = r_in - n_text_ct;
     t.q_row0 = tt * 128;
     t.rows_valid = min((int64_t)128, g.Tv - t.q_row0);
-    t.count = P.ws.tile_count[t.h * P.video_tiles_per_head + tt];
-    t.list = P.ws.tile_list + (t.h * P.video_tiles_per_head + tt) * g.M;
+    if (g.B == 128) {   // one query block per tile: its own kv list (tile_lists skipped)
+      t.count = P.ws.kv_count[t.h * g.N + tt];
+      t.list = P.ws.kv_list + (t.h * g.N + tt) * g.M;
+    } else {
+      t.count = P.ws.tile_count[t.h * P.video_tiles_per_head + tt];
+      t.list = P.ws.tile_list + (t.h * P.video_tiles_per_head + tt) * g.M;
+    }
   }
   return t;
 }
@@ -797,7 +807,7 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
         if (t.list) {
           const int32_t e = t.list[j];
           m = e & 0xFFFFFF;
-          member = (e >> (24 + sub)) & 1;
+          member = BKV == 128 || ((e >> (24 + sub)) & 1);   // plain kv-list entries at B = 128
         } else {
           m = t.m_first + j;
           member = true;

@@ -949,6 +949,8 @@ cudaError_t launch_lists_from_mask(const Geometry& g, const uint8_t* mask, const
 
 cudaError_t launch_tile_lists(const Geometry& g, const Workspace& ws, cudaStream_t st,
                               int* launches) {
+  // B = 128: a 128-row tile is one query block, K3 walks its kv list directly
+  if (g.B == kTcTileRows) return cudaSuccess;
   const int64_t G = kTcTileRows / g.B;
   const int64_t tiles = g.H * ((g.N + G - 1) / G);
   const int64_t threads = tiles * 32;

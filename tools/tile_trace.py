@@ -31,7 +31,7 @@ torch.cuda.synchronize()
 st = lse[:2048].view(torch.int64).view(256, 4).cpu().numpy()
 L = nat.layout(shape)
 vt = 928
-tc = ws[L["tile_count"]:L["tile_count"] + heads * vt * 4].view(torch.int32).cpu().numpy()
+tc = ws[L["kv_count"]:L["kv_count"] + heads * vt * 4].view(torch.int32).cpu().numpy()   # B = 128: tile = block
 cta, grid, tph = int(os.environ["RSA_TC_TRACE_CTA"]), 148, 16 + vt
 rows = []
 for i in range(256):
