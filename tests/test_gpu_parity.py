@@ -418,3 +418,22 @@ def test_select_rows_max_kv_blocks(p):
         # one block more than the bound
         run_np(np.concatenate([qv, qv[:8]]), qt, np.concatenate([k, k[:8]]), np.concatenate([v, v[:8]]),
                block, 0.1, p, 0, False, "sparse-rectified")
+
+
+@pytest.mark.parametrize("d,block", [(64, 64), (128, 128)])
+@pytest.mark.parametrize("scale_range", [0, 24])
+def test_bf16_pooling_bit_exact(scale_range, d, block):
+    """K1's bf16 path (fp64 sums proven exact by the block's magnitude range,
+    TwoSum otherwise) reproduces math.fsum means bit for bit; scale_range > 0
+    spreads the rows over 2^+-scale_range so the range test and its fallback run."""
+    rng = np.random.default_rng(17)
+    t_v, t_t = block * 24, 100
+    qv, qt, k, v = (O.round_to_bf16(x) for x in O.random_problem(3, t_v=t_v, t_t=t_t, d=d, dtype=np.float32))
+    if scale_range:
+        sc = lambda x: O.round_to_bf16(x * np.exp2(rng.integers(-scale_range, scale_range + 1, size=(x.shape[0], 1))))
+        qv, qt, k, v = sc(qv), sc(qt), sc(k), sc(v)
+    res = rsa.rectified_attention_pipeline(bf16_problem(qv, qt, k, v, block), SparsityConfig(0.2, 0.0, 0, False))
+    ref = O.pool(qv, k, v, t_t, block)
+    np.testing.assert_array_equal(res.pooled.q_pool.cpu().numpy(), ref["q_pool"])
+    np.testing.assert_array_equal(res.pooled.v_pool.cpu().numpy(), ref["v_pool"])
+    np.testing.assert_array_equal(res.pooled.k_mix_pool.cpu().numpy(), ref["k_mix"])
