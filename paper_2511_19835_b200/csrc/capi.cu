@@ -485,6 +485,7 @@ rsa_status rsa_check_device_status(void* workspace, void* stream) {
   cudaError_t e = cudaMemcpyAsync(flags, workspace, sizeof(flags), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "status readback");
+  if (flags[rsa::ST_NONFINITE]) return fail(RSA_ERR_SHAPE, "q/k/v contain non-finite entries");
   if (flags[rsa::ST_DEGENERATE])
     return fail(RSA_ERR_DEGENERATE_ROW, "reallocation denominator is zero on some rows");
   if (flags[rsa::ST_EMPTY_ROW]) return fail(RSA_ERR_EMPTY_ROW, "a mask row retains no key block");

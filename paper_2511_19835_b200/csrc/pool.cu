@@ -16,6 +16,8 @@
 // independent of launch geometry.
 #include "rsa_internal.cuh"
 
+#include <cfloat>
+
 #include <algorithm>
 
 namespace rsa {
@@ -96,6 +98,7 @@ pool_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restric
   __shared__ float s_amax[kThreads / 32], s_amin[kThreads / 32];
   __shared__ int s_exact;
   bool exact = false;
+  bool nonfinite = false;
   if constexpr (kTryPlain) {
     double acc[VEC];
     float amax = 0.f, amin = INFINITY;
@@ -113,6 +116,7 @@ pool_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restric
           for (int i = 0; i < VEC; ++i) {
             acc[i] += (double)x[u][i];
             const float ax = fabsf(x[u][i]);
+            nonfinite |= !(ax <= FLT_MAX);
             amax = fmaxf(amax, ax);
             amin = fminf(amin, ax > 0.f ? ax : INFINITY);
           }
@@ -129,6 +133,7 @@ pool_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restric
         for (int i = 0; i < VEC; ++i) {
           acc[i] += (double)x[i];
           const float ax = fabsf(x[i]);
+          nonfinite |= !(ax <= FLT_MAX);
           amax = fmaxf(amax, ax);
           amin = fminf(amin, ax > 0.f ? ax : INFINITY);
         }
@@ -169,6 +174,7 @@ pool_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restric
         load_vec<T, VEC>(src + r * d + c * VEC, x);
 #pragma unroll
         for (int i = 0; i < VEC; ++i) {
+          nonfinite |= !(fabs(x[i]) <= DBL_MAX);
           double sm, e;
           two_sum(hi[i], x[i], sm, e);
           hi[i] = sm;
@@ -186,6 +192,7 @@ pool_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restric
       }
     }
   }
+  if (nonfinite) atomicOr(ws.status + ST_NONFINITE, 1);
   __syncthreads();
 
   for (int64_t col = t; col < d; col += kThreads) {
@@ -417,6 +424,7 @@ pool_bulk_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
         mx = max(mx, reinterpret_cast<uint32_t*>(s_rng)[2 * w]);
         mn = min(mn, reinterpret_cast<uint32_t*>(s_rng)[2 * w + 1]);
       }
+      if (mx >= 0x7F80u) atomicOr(ws.status + ST_NONFINITE, 1);   // exponent field 0xFF: inf / NaN
       int lg = 0;
       while ((int64_t(1) << lg) < len) ++lg;
       // exponent fields (bits >> 7); subnormals (field 0) count as exponent 1

@@ -65,7 +65,9 @@ enum MaskBit : uint8_t {
   BIT_MASK = 1, BIT_IMPORTANCE = 2, BIT_COMP = 4, BIT_ADJ = 8, BIT_APPLIED = 16
 };
 
-enum StatusFlag { ST_DEGENERATE = 0, ST_EMPTY_ROW = 1, ST_DEFICIT = 2 };
+// ST_NONFINITE: K1 saw an inf / NaN in Q, K or V (the reference's
+// check_matrix ShapeError, core.py:23-31, folded into the pooling pass)
+enum StatusFlag { ST_DEGENERATE = 0, ST_EMPTY_ROW = 1, ST_DEFICIT = 2, ST_NONFINITE = 3 };
 
 constexpr int kTcTileRows = 128;   // query rows per tcgen05 tile (UMMA M)
 

@@ -437,3 +437,25 @@ def test_bf16_pooling_bit_exact(scale_range, d, block):
     np.testing.assert_array_equal(res.pooled.q_pool.cpu().numpy(), ref["q_pool"])
     np.testing.assert_array_equal(res.pooled.v_pool.cpu().numpy(), ref["v_pool"])
     np.testing.assert_array_equal(res.pooled.k_mix_pool.cpu().numpy(), ref["k_mix"])
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32, torch.float64])
+@pytest.mark.parametrize("where", ["q_video", "k", "v"])
+def test_non_finite_inputs_raise_shape_error(dtype, where):
+    """core.py:23-31 (check_matrix): inf / NaN in q/k/v is a ShapeError.  For
+    CUDA tensors K1 flags it while pooling; the pipeline and the batched op
+    (check_status=True) raise it from the device status."""
+    qv, qt, k, v = O.random_problem(2, t_v=64 * 4, t_t=10, d=64, dtype=np.float32)
+    arrs = {"q_video": qv, "q_text": qt, "k": k, "v": v}
+    bad = arrs[where].copy()
+    bad[5, 7] = np.nan if where != "v" else np.inf
+    arrs[where] = bad
+    t = {n: torch.from_numpy(a).to(dtype).cuda() for n, a in arrs.items()}
+    prob = AttentionProblem(q_video=t["q_video"], q_text=t["q_text"], k=t["k"], v=t["v"], d=64, block=64)
+    with pytest.raises(rsa.ShapeError):
+        rsa.rectified_attention_pipeline(prob, SparsityConfig(0.5, 0.0, 0, False))
+    if dtype == torch.bfloat16:
+        q = torch.cat([t["q_video"], t["q_text"]])[None]
+        with pytest.raises(rsa.ShapeError):
+            rsa.rectified_sparse_attention(q, t["k"][None], t["v"][None], num_text_tokens=10, block=64,
+                                           sparsity=0.5, check_status=True)
