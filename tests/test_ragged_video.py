@@ -147,3 +147,31 @@ def test_gpu_ragged_hunyuan_exact_token_count():
     np.testing.assert_array_equal(res.sparse_mask.mask.cpu().numpy(), sel["mask"])
     np.testing.assert_allclose(res.implicit.a_pool.cpu().numpy(), imp["a_pool"], atol=1e-12, rtol=0)
     assert torch.equal(res.output.o_video, out[0, 0, :t_v])
+
+
+@pytest.mark.gpu
+def test_gpu_ragged_fused_morton_matches_oracle():
+    """Ragged final video block + fused Morton reorder (K1 gather, K3 scatter):
+    the reordered problem's masks bit-exact against the oracle's extension,
+    outputs back in the original token order within the bf16 bar."""
+    from paper_2511_19835_b200.pipeline import workspace_for
+    grid, block, d, t_t = (3, 10, 9), 64, 64, 70
+    t_v = grid[0] * grid[1] * grid[2]                # 270 = 4 * 64 + 14
+    qv, qt, k, v = (O.round_to_bf16(x) for x in O.random_problem(21, t_v=t_v, t_t=t_t, d=d, dtype=np.float32))
+    q = torch.cat([_bf16(qv), _bf16(qt)])[None]
+    shape = nat.make_shape(1, t_v, t_t, d, block, "bfloat16", ragged_video=True)
+    ws = workspace_for(shape, "cuda")
+    out = rsa.rectified_sparse_attention(q, _bf16(k)[None], _bf16(v)[None], num_text_tokens=t_t, block=block,
+                                         top_k_fraction=0.4, grid_dims=grid, morton=True, workspace=ws,
+                                         check_status=True, ragged_video=True)[0]
+    rq, rqt, rk, rv, perm = O.reorder_morton(qv, qt, k, v, grid)
+    ref = O.pipeline(rq, rqt, rk, rv, block, 0.4, 0.0, 0, False, "sparse-rectified", ragged=True)
+    L = nat.layout(shape)
+    n, m = ref["mask"].shape
+    bits = ws[L["mask_bits"]:L["mask_bits"] + n * m].view(n, m).cpu().numpy()
+    np.testing.assert_array_equal((bits & 1) != 0, ref["mask"])
+    want = np.empty((t_v + t_t, d), np.float64)
+    want[perm] = ref["o_video"]
+    want[t_v:] = ref["o_text"]
+    got = out.float().cpu().numpy().astype(np.float64)
+    assert np.abs(got - want).max() <= 2e-2 and O.cosine(got, want) >= 0.999
