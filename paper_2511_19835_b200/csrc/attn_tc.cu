@@ -705,6 +705,10 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
 
   const Geometry& g = P.g;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // RSA_TC_STAMPS=4: per-CTA globaltimer at start / end into `lse` (load-balance profiling)
+  unsigned long long* cta_stamp =
+      (P.stamps == 4 && P.lse) ? reinterpret_cast<unsigned long long*>(P.lse) + 2 * blockIdx.x : nullptr;
+  if (cta_stamp && threadIdx.x == 0) cta_stamp[0] = gtimer();
 
   if (threadIdx.x == 0) {
     ptx::mbar_init(q_full, 128 * WPQ);
@@ -976,6 +980,7 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
   __syncwarp();
   ptx::tc_fence_before();
   __syncthreads();
+  if (cta_stamp && threadIdx.x == 0) cta_stamp[1] = gtimer();
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<C::TMEM_COLS>(tmem);
