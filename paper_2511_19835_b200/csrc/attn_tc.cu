@@ -80,6 +80,8 @@ struct TcParams {
   int trace_cta;     // CTA traced per step when stamps == 2
   int stamps;        // RSA_TC_STAMPS=1: per-CTA globaltimer stamps into `lse` (profiling)
   int qring;         // persistent kernel: each tile's Q rows arrive by TMA in a K/V ring stage
+  int mma_spin;      // persistent kernel: the MMA warp polls P (no try_wait suspend)
+  int sm_spin;       // persistent kernel: the softmax warps poll S
   int mode;          // 0 normal; diagnostics: 1 no softmax math, 2 TMA only, 3 MMA only, 4 MMA+TMA,
                      // 6 softmax only, 7 normal + per-CTA globaltimer stamps into `lse`
 };
@@ -663,7 +665,8 @@ __device__ __forceinline__ void mma_loop(const CUtensorMap& tm_k, const CUtensor
       }
       if (j >= 1) {
         const int64_t gj = gs + j - 1;
-        ptx::mbar_wait(p_full + (gj % C::NS), (uint32_t)((gj / C::NS) & 1));
+        if (P.mma_spin) ptx::mbar_spin(p_full + (gj % C::NS), (uint32_t)((gj / C::NS) & 1));
+        else ptx::mbar_wait(p_full + (gj % C::NS), (uint32_t)((gj / C::NS) & 1));
         ptx::mbar_wait(kv_full + s_kv, ph_kv);
         ptx::tc_fence_after();
         const uint32_t a_tmem = tm + (uint32_t)((gj % C::NS) * BKV);
@@ -817,7 +820,8 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
           member = true;
         }
         const int len = (int)kv_len(g, m);
-        ptx::mbar_wait(s_full + (gj % C::NS), (uint32_t)((gj / C::NS) & 1));
+        if (P.sm_spin) ptx::mbar_spin(s_full + (gj % C::NS), (uint32_t)((gj / C::NS) & 1));
+        else ptx::mbar_wait(s_full + (gj % C::NS), (uint32_t)((gj / C::NS) & 1));
         if (tt && j == 0 && tix < 256) tt[tix * 4 + 0] = clock64();
         ptx::tc_fence_after();
         const uint32_t s_addr = lane_base + (uint32_t)((gj % C::NS) * BKV);
@@ -1102,6 +1106,9 @@ cudaError_t launch_persistent(const Geometry& g, const void* q, const void* k, c
   // are not gathered through a permutation; RSA_TC_QRING=0 loads Q rows directly
   static const int qring_env = [] { const char* e = getenv("RSA_TC_QRING"); return e ? atoi(e) : 1; }();
   P.qring = (qring_env != 0 && C::STAGE == C::Q_BYTES && perm == nullptr) ? 1 : 0;
+  static const int spin_env = [] { const char* e = getenv("RSA_TC_SPIN"); return e ? atoi(e) : 0; }();
+  P.mma_spin = spin_env & 1;
+  P.sm_spin = (spin_env >> 1) & 1;
   P.g = g;
   P.ws = ws;
   P.out = static_cast<__nv_bfloat16*>(out);
