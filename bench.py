@@ -510,6 +510,22 @@ def run_ours(args):
         "gpu_launches": launches_per_step * args.steps,
         "e2e": e2e,
     }
+    # the other two stages against their own bounds: K1 streams Q/K/V
+    # once from HBM; K2 is fp64 GEMM + per-row work (neither HBM- nor tensor-bound)
+    t_all = cfg["t_v"] + cfg["t_t"]
+    k1_bytes = (cfg["t_v"] + 2 * t_all) * d * 2 * heads
+    n_q, n_cols = grid.n_q, grid.n_cols
+    k2_flop = (2 * n_q * n_cols * d + 2 * n_q * grid.n_kv * d) * heads
+    if stage.get("pool") and stage.get("select"):
+        line["stage_rooflines"] = {
+            "K1_pool": {"bound": "hbm", "achieved": k1_bytes / (stage["pool"] * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
+                        "unit": "GB/s", "frac": k1_bytes / (stage["pool"] * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                        "algorithmic": f"{k1_bytes / 1e9:.3f} GB read per launch ((T_v + 2T) * d * 2 per head)"},
+            "K2_select": {"bound": "fp64 GEMM + per-row", "achieved": k2_flop / (stage["select"] * 1e-3) / 1e12,
+                          "peak": None, "unit": "fp64 TFLOP/s",
+                          "algorithmic": f"{k2_flop / 1e9:.2f} GFLOP fp64 per launch (scores + compensation GEMMs); "
+                                         "peak: ~37 TF/s fp64 datasheet, unmeasured"},
+        }
     if not args.profile:
         line["clocks"] = clocks.summary()
     if world == 1 and not args.no_cpu_baseline and not args.profile:
