@@ -684,6 +684,10 @@ __device__ __forceinline__ void mma_loop(const CUtensorMap& tm_k, const CUtensor
         advance();
       }
     }
+    // the epilogue waits for this (one phase per tile: a per-PV parity wait is
+    // exact only one phase ahead, and PV_{count-2} can still be running there)
+    if (ptx::elect_one()) ptx::tc_commit(pv_done + 1);
+    __syncwarp();
     gs += count;
   }
 }
@@ -703,7 +707,8 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
   uint64_t* s_full = kv_empty + C::NST;    // [NS]
   uint64_t* p_full = s_full + C::NS;       // [NS]
   uint64_t* pv_done = p_full + C::NS;      // [1]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 1);
+  uint64_t* o_full = pv_done + 1;          // [1] a tile's last PV is complete (one phase per tile)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
   float* red_max = reinterpret_cast<float*>(bars + 32);   // [2][WPQ][128] row maxima + [WPQ][128] row sums
 
   const Geometry& g = P.g;
@@ -724,6 +729,7 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
       ptx::mbar_init(p_full + i, 128 * WPQ);
     }
     ptx::mbar_init(pv_done, 1);
+    ptx::mbar_init(o_full, 1);
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc<C::TMEM_COLS>(tmem_slot);
@@ -911,10 +917,8 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
       float l_run = 0.f;
 #pragma unroll
       for (int p2 = 0; p2 < WPQ; ++p2) l_run += red_max[2 * WPQ * 128 + p2 * 128 + row];
-      if (count > 0) {
-        ptx::mbar_wait(pv_done, (uint32_t)((gs + count - 1) & 1));
-        ptx::tc_fence_after();
-      }
+      ptx::mbar_wait(o_full, (uint32_t)(tix & 1));   // every PV of this tile is complete
+      ptx::tc_fence_after();
       const bool valid = row < cur.rows_valid;
       const int64_t grow = cur.q_row0 + row;
       if (cur.text) {
@@ -1092,6 +1096,391 @@ bool make_tmap_3d(CUtensorMap* tm, const void* ptr, int64_t dim0, int64_t dim1, 
   return r == CUDA_SUCCESS;
 }
 
+// ============================================================================
+// Ping-pong kernel (default for d = B = 128; RSA_TC_PP=0 disables): two query tiles per CTA in
+// independent "slots", FA4-style.  Each slot has its own Q (shared memory, SS
+// MMA for S), K/V ring, S/P and O TMEM columns (2 x (128 + 128) = 512), TMA
+// producer warp, MMA warp and softmax warpgroup with one thread per row (no
+// row-max exchange), so one slot's softmax overlaps the other slot's MMAs and
+// the MUFU pipe is fed by whichever slot is in its ex2 phase; a slot's
+// epilogue overlaps the other slot's steps.  d = B = 128 only.
+// Warps: 0/1 TMA producers (slot 0/1), 2/3 MMA issuers, 4-7 / 8-11 softmax.
+// ============================================================================
+struct CfgPP {
+  static constexpr int D = 128, BKV = 128;
+  static constexpr int NST = 2;                   // K/V stages per slot
+  static constexpr int STAGE = BKV * D * 2;       // 32 KB
+  static constexpr int KV_PANEL = BKV * 128;      // 16 KB: 128 rows x 128 B
+  static constexpr int Q_PANEL = 128 * 128;
+  static constexpr int Q_BYTES = 128 * D * 2;     // 32 KB
+  static constexpr int SLOT_SMEM = Q_BYTES + NST * STAGE;
+  static constexpr int SMEM = 1024 + 2 * SLOT_SMEM + 512;
+  static constexpr uint32_t IDESC_S64 = ptx::idesc_bf16(128, 64, false);   // S sub-steps: 64 keys
+  static constexpr uint32_t IDESC_O = ptx::idesc_bf16(128, D, true);   // V MN-major
+  static constexpr int THREADS = 384;
+};
+
+__global__ void __launch_bounds__(384, 1)
+attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                  const __grid_constant__ CUtensorMap tm_v, const TcParams P, int64_t n_tiles) {
+  using C = CfgPP;
+  constexpr int D = C::D, BKV = C::BKV;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + 2 * C::SLOT_SMEM);
+  // per slot: q_full, q_empty, kv_full[2], kv_empty[2], s_full[2], pv_done, p_full[2], o_full  (12 barriers)
+  auto slot_bar = [&](int s, int i) { return bars + s * 12 + i; };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
+
+  const Geometry& g = P.g;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; ++s) {
+      ptx::mbar_init(slot_bar(s, 0), 1);     // q_full (TMA)
+      ptx::mbar_init(slot_bar(s, 1), 1);     // q_empty (MMA commit after a tile's last S)
+      for (int i = 0; i < 2; ++i) {
+        ptx::mbar_init(slot_bar(s, 2 + i), 1);   // kv_full
+        ptx::mbar_init(slot_bar(s, 4 + i), 1);   // kv_empty
+      }
+      ptx::mbar_init(slot_bar(s, 6), 1);     // s_full[0]
+      ptx::mbar_init(slot_bar(s, 7), 1);     // s_full[1]
+      ptx::mbar_init(slot_bar(s, 8), 1);     // pv_done
+      ptx::mbar_init(slot_bar(s, 9), 128);   // p_full[0]
+      ptx::mbar_init(slot_bar(s, 10), 128);  // p_full[1]
+      ptx::mbar_init(slot_bar(s, 11), 1);    // o_full: the tile's last PV is complete
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc<512>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // slot s walks tiles (blockIdx.x + k * gridDim.x) * 2 + s
+  const int64_t stride = 2 * (int64_t)gridDim.x;
+
+  if (warp < 2) {
+    // ===================== TMA producer of slot `warp` =====================
+    const int s = warp;
+    if (lane == 0) {
+      ptx::prefetch_tmap(&tm_q);
+      ptx::prefetch_tmap(&tm_k);
+      ptx::prefetch_tmap(&tm_v);
+      const uint64_t keep = ptx::policy_evict_last();
+      uint8_t* qs = base + s * C::SLOT_SMEM;
+      uint8_t* ring = qs + C::Q_BYTES;
+      int st = 0;
+      uint32_t ph = 0, qph = 0;
+      for (int64_t bid = 2 * (int64_t)blockIdx.x + s; bid < n_tiles; bid += stride) {
+        const TileDesc t = decode_tile(P, bid);
+        ptx::mbar_wait(slot_bar(s, 1), qph ^ 1);    // previous tile's S MMAs have read Q
+        qph ^= 1;
+        ptx::mbar_expect_tx(slot_bar(s, 0), C::Q_BYTES);
+#pragma unroll
+        for (int p = 0; p < 2; ++p)
+          ptx::tma_load_3d(qs + p * C::Q_PANEL, &tm_q, slot_bar(s, 0), 64 * p, (int)t.q_row0, (int)t.h);
+        for (int64_t j = 0; j < t.count; ++j) {
+          const int64_t m = t.list ? (t.list[j] & 0xFFFFFF) : t.m_first + j;
+#pragma unroll
+          for (int kv = 0; kv < 2; ++kv) {
+            ptx::mbar_wait(slot_bar(s, 4 + st), ph ^ 1);
+            ptx::mbar_expect_tx(slot_bar(s, 2 + st), C::STAGE);
+            uint8_t* dst = ring + st * C::STAGE;
+#pragma unroll
+            for (int p = 0; p < 2; ++p)
+              ptx::tma_load_3d_hint(dst + p * C::KV_PANEL, kv ? &tm_v : &tm_k, slot_bar(s, 2 + st), 64 * p,
+                                    (int)kv_row0(g, m), (int)t.h, keep);
+            if (++st == C::NST) { st = 0; ph ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp < 4) {
+    // ===================== MMA issuer of slot `warp - 2` =====================
+    // 64-key sub-steps i (two per kv block) into S buffers i % 2 ([0,64) and
+    // [64,128) of the slot's S columns): S_{i+1} runs while the softmax works
+    // on S_i; S_{i+2} reuses buffer i % 2 after PV_i (in-order tensor pipe).
+    const int s = warp - 2;
+    const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0) + (uint32_t)(s * 256);
+    const uint32_t q_addr = __shfl_sync(0xffffffffu, ptx::smem_u32(base + s * C::SLOT_SMEM), 0);
+    const uint32_t ring = q_addr + C::Q_BYTES;
+    int st = 0;          // ring stage of the current kv block's K (V is the next stage)
+    uint32_t ph = 0, qph = 0;
+    int64_t gi = 0;      // sub-steps before the current tile
+    auto stage_of = [&](int64_t blk_in_tile, int kv, int& st_out, uint32_t& ph_out) {
+      // K_j and V_j occupy consecutive ring slots: index 2j (+1)
+      const int64_t idx = 2 * blk_in_tile + kv;
+      (void)idx;
+      st_out = st;
+      ph_out = ph;
+    };
+    (void)stage_of;
+    for (int64_t bid = 2 * (int64_t)blockIdx.x + s; bid < n_tiles; bid += stride) {
+      const int64_t count = decode_tile(P, bid).count;
+      const int64_t nsub = 2 * count;
+      ptx::mbar_wait(slot_bar(s, 0), qph);
+      qph ^= 1;
+      ptx::tc_fence_after();
+      // ring bookkeeping: block j's K at stage kst(j), V at the next stage
+      int k_st = st;
+      uint32_t k_ph = ph;
+      auto issue_s = [&](int64_t i) {       // S_i, i = 2 j + half
+        const int64_t j = i >> 1;
+        const int half = (int)(i & 1);
+        int kst = k_st;
+        uint32_t kph = k_ph;
+        // K of block j: ring slot (st0 + 2 j) mod NST
+        const int64_t slot = (int64_t)kst + 2 * j;
+        const int sj = (int)(slot % C::NST);
+        const uint32_t pj = kph ^ (uint32_t)((slot / C::NST) & 1);
+        if (half == 0) ptx::mbar_wait(slot_bar(s, 2 + sj), pj);
+        ptx::tc_fence_after();
+        const uint32_t kb = ring + (uint32_t)(sj * C::STAGE) + (uint32_t)(half * 64 * 128);
+        const uint32_t d_tmem = tm + (uint32_t)(half * 64);
+        if (ptx::elect_one()) {
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k) {
+            const uint32_t off = (uint32_t)((k / 4) * C::Q_PANEL + (k % 4) * 32);
+            const uint64_t a = ptx::sw128_desc(q_addr + off, 16, 1024);
+            const uint64_t b = ptx::sw128_desc(kb + (k / 4) * C::KV_PANEL + (k % 4) * 32, 16, 1024);
+            ptx::mma_ss(d_tmem, a, b, C::IDESC_S64, k > 0);
+          }
+          if (half == 1) ptx::tc_commit(slot_bar(s, 4 + sj));   // K_j fully read
+          ptx::tc_commit(slot_bar(s, 6 + half));                  // s_full[half]
+          if (i == nsub - 1) ptx::tc_commit(slot_bar(s, 1));      // Q may be replaced after this
+        }
+        __syncwarp();
+      };
+      if (nsub > 0) issue_s(0);
+      if (nsub > 1) issue_s(1);
+      for (int64_t i = 0; i < nsub; ++i) {
+        const int64_t gsub = gi + i;
+        const int64_t j = i >> 1;
+        const int half = (int)(i & 1);
+        // O += P_i V_i[64 half rows] once the softmax has written P_i
+        ptx::mbar_wait(slot_bar(s, 9 + half), (uint32_t)((gsub >> 1) & 1));
+        const int64_t slot = (int64_t)k_st + 2 * j + 1;
+        const int sv = (int)(slot % C::NST);
+        const uint32_t pv = k_ph ^ (uint32_t)((slot / C::NST) & 1);
+        if (half == 0) ptx::mbar_wait(slot_bar(s, 2 + sv), pv);
+        ptx::tc_fence_after();
+        const uint32_t vb = ring + (uint32_t)(sv * C::STAGE) + (uint32_t)(half * 64 * 128);
+        if (ptx::elect_one()) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t b = ptx::sw128_desc(vb + k * 2048, C::KV_PANEL, 1024);
+            ptx::mma_ts(tm + 128, tm + (uint32_t)(half * 64) + k * 8, b, C::IDESC_O, (i > 0 || k > 0) ? 1u : 0u);
+          }
+          if (half == 1) ptx::tc_commit(slot_bar(s, 4 + sv));   // V_j fully read
+          ptx::tc_commit(slot_bar(s, 8));                         // pv_done
+        }
+        __syncwarp();
+        if (i + 2 < nsub) issue_s(i + 2);
+      }
+      if (ptx::elect_one()) ptx::tc_commit(slot_bar(s, 11));   // one phase per tile, for the epilogue
+      __syncwarp();
+      // advance the ring past this tile's 2 * count stages
+      const int64_t used = (int64_t)st + 2 * count;
+      ph ^= (uint32_t)((used / C::NST) & 1);
+      st = (int)(used % C::NST);
+      gi += nsub;
+    }
+  } else {
+    // ===================== softmax + epilogue of slot s, one thread per row =====================
+    const int s = (warp - 4) >> 2;
+    const int quad = warp & 3;
+    const int row = quad * 32 + lane;
+    const uint32_t lane_base = tmem + (uint32_t)(s * 256) + ((uint32_t)(quad * 32) << 16);
+    const float sl2 = P.scale_log2;
+    const uint64_t once = ptx::policy_evict_first();
+    int64_t gi = 0;
+    int64_t tix_s = 0;   // tiles of this slot so far (o_full phases)
+    for (int64_t bid = 2 * (int64_t)blockIdx.x + s; bid < n_tiles; bid += stride) {
+      const TileDesc t = decode_tile(P, bid);
+      const int64_t count = t.count, nsub = 2 * count;
+      float m_run = -INFINITY, l_run = 0.f;
+      for (int64_t i = 0; i < nsub; ++i) {
+        const int64_t gsub = gi + i;
+        const int half = (int)(i & 1);
+        const int64_t m = t.list ? (t.list[i >> 1] & 0xFFFFFF) : t.m_first + (i >> 1);
+        const int blen = (int)kv_len(g, m);
+        const int len = blen - half * 64;
+        ptx::mbar_wait(slot_bar(s, 6 + half), (uint32_t)((gsub >> 1) & 1));
+        ptx::tc_fence_after();
+        const uint32_t sbuf = lane_base + (uint32_t)(half * 64);
+        uint32_t sr[2][32];
+        ptx::tmem_ld32(sbuf, sr[0]);
+        ptx::tmem_ld32(sbuf + 32, sr[1]);
+        ptx::tmem_ld_wait();
+        if (len < 64) {
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int q2 = 0; q2 < 32; ++q2)
+              if (c * 32 + q2 >= len) sr[c][q2] = __float_as_uint(-INFINITY);
+        }
+        float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int q2 = 0; q2 < 32; ++q2) mx4[q2 & 3] = fmaxf(mx4[q2 & 3], __uint_as_float(sr[c][q2]));
+        const float m_blk = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * sl2;
+        float alpha = 1.f;
+        bool rescale_o = false;
+        if (m_blk > m_run + kRescaleThreshold || (m_run == -INFINITY && m_blk > -INFINITY)) {
+          alpha = (m_run == -INFINITY) ? 0.f : ptx::ex2(m_run - m_blk);
+          rescale_o = (m_run != -INFINITY) && i > 0;
+          m_run = m_blk;
+        }
+        const float base_m = (m_run == -INFINITY) ? 0.f : m_run;
+        const float2 sc2 = make_float2(sl2, sl2), nb2 = make_float2(-base_m, -base_m);
+        float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int q2 = 0; q2 < 16; ++q2) {
+            const float2 x = ptx::ffma2(make_float2(__uint_as_float(sr[c][2 * q2]), __uint_as_float(sr[c][2 * q2 + 1])),
+                                        sc2, nb2);
+            const float2 p = make_float2(ptx::ex2(x.x), ptx::ex2(x.y));
+            sum2[q2 & 1] = ptx::fadd2(sum2[q2 & 1], p);
+            pk[q2] = ptx::pack_bf16(p.x, p.y);
+          }
+          ptx::tmem_st16(sbuf + c * 16, pk);
+        }
+        const float2 st2 = ptx::fadd2(sum2[0], sum2[1]);
+        l_run = l_run * alpha + (st2.x + st2.y);
+        if (__any_sync(0xffffffffu, rescale_o)) {
+          ptx::mbar_wait(slot_bar(s, 8), (uint32_t)((gsub - 1) & 1));   // O = PV_..i-1
+          ptx::tc_fence_after();
+          const float a = rescale_o ? alpha : 1.f;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t o[32];
+            const uint32_t oa = lane_base + 128 + c * 32;
+            ptx::tmem_ld32(oa, o);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int q2 = 0; q2 < 32; ++q2) o[q2] = __float_as_uint(__uint_as_float(o[q2]) * a);
+            ptx::tmem_st32(oa, o);
+          }
+        }
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(slot_bar(s, 9 + half));
+      }
+      // ---- epilogue (overlaps the other slot's steps) ----
+      // every PV of this tile is complete (one o_full phase per tile: a per-PV
+      // parity wait is exact only one phase ahead, and the last two PVs -- both
+      // halves of the last block -- can still be in flight here)
+      ptx::mbar_wait(slot_bar(s, 11), (uint32_t)(tix_s & 1));
+      ptx::tc_fence_after();
+      ++tix_s;
+      const bool valid = row < t.rows_valid;
+      const int64_t grow = t.q_row0 + row;
+      if (t.text) {
+        float* po = P.text_part + (t.part * 128 + row) * D;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t o[32];
+          ptx::tmem_ld32(lane_base + 128 + c * 32, o);
+          ptx::tmem_ld_wait();
+          if (valid) {
+#pragma unroll
+            for (int v4 = 0; v4 < 8; ++v4)
+              *reinterpret_cast<uint4*>(po + c * 32 + v4 * 4) =
+                  make_uint4(o[v4 * 4], o[v4 * 4 + 1], o[v4 * 4 + 2], o[v4 * 4 + 3]);
+          }
+        }
+        if (valid) P.text_ml[t.part * 128 + row] = make_float2(m_run, l_run);
+      } else {
+        float rfac = 1.f;
+        const double* comp = nullptr;
+        if (P.rectify && valid) {
+          const int64_t n_blk = grow / g.B;
+          rfac = P.ws.r_eff[t.h * g.N + n_blk];
+          comp = P.ws.comp + (t.h * g.N + n_blk) * D;
+        }
+        const float inv_l = (nsub > 0 && l_run > 0.f) ? 1.f / l_run : 0.f;
+        __nv_bfloat16* orow = P.out + (t.h * g.T + grow) * D;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t o[32];
+          ptx::tmem_ld32(lane_base + 128 + c * 32, o);
+          ptx::tmem_ld_wait();
+          if (valid) {
+#pragma unroll
+            for (int v8 = 0; v8 < 4; ++v8) {
+              uint32_t w[4];
+#pragma unroll
+              for (int q2 = 0; q2 < 4; ++q2) {
+                const int col = c * 32 + v8 * 8 + 2 * q2;
+                float y0 = inv_l == 0.f ? 0.f : __uint_as_float(o[v8 * 8 + 2 * q2]) * inv_l * rfac;
+                float y1 = inv_l == 0.f ? 0.f : __uint_as_float(o[v8 * 8 + 2 * q2 + 1]) * inv_l * rfac;
+                if (comp) {
+                  y0 += (float)comp[col];
+                  y1 += (float)comp[col + 1];
+                }
+                w[q2] = ptx::pack_bf16(y0, y1);
+              }
+              ptx::st_stream(orow + c * 32 + v8 * 8, make_uint4(w[0], w[1], w[2], w[3]), once);
+            }
+          }
+        }
+        if (valid && P.lse)
+          P.lse[t.h * g.T + grow] = l_run > 0.f ? (log2f(l_run) + m_run) * 0.69314718055994531f : -INFINITY;
+      }
+      ptx::tc_fence_before();
+      gi += nsub;
+    }
+  }
+
+  __syncwarp();
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tmem);
+  }
+}
+
+cudaError_t launch_pp(const Geometry& g, const void* q, const void* k, const void* v, void* out, float* lse,
+                      const Workspace& ws, bool rectify, bool text, cudaStream_t st) {
+  using C = CfgPP;
+  CUtensorMap tq, tk, tv;
+  if (!make_tmap_3d(&tq, q, g.d, g.T, g.H, 128) || !make_tmap_3d(&tk, k, g.d, g.T, g.H, 128) ||
+      !make_tmap_3d(&tv, v, g.d, g.T, g.H, 128))
+    return cudaErrorInvalidValue;
+  TcParams P{};
+  P.g = g;
+  P.ws = ws;
+  P.out = static_cast<__nv_bfloat16*>(out);
+  P.q = static_cast<const __nv_bfloat16*>(q);
+  P.lse = lse;
+  P.rectify = rectify ? 1 : 0;
+  P.text_tiles_per_head = text ? (g.Tt + 127) / 128 : 0;
+  P.text_chunks = text_chunks(g);
+  P.chunk_blocks = (g.M + P.text_chunks - 1) / P.text_chunks;
+  P.video_tiles_per_head = (g.N * g.B + 127) / 128;
+  P.tiles_per_head = P.text_tiles_per_head * P.text_chunks + P.video_tiles_per_head;
+  P.text_part = ws.text_part;
+  P.text_ml = reinterpret_cast<float2*>(ws.text_ml);
+  P.scale_log2 = (float)(1.4426950408889634 / sqrt((double)g.d));
+  cudaError_t e = cudaFuncSetAttribute(attn_tc_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t n_tiles = g.H * P.tiles_per_head;
+  attn_tc_pp_kernel<<<(unsigned)std::min<int64_t>((n_tiles + 1) / 2, sms), C::THREADS, C::SMEM, st>>>(tq, tk, tv, P,
+                                                                                                        n_tiles);
+  e = cudaGetLastError();
+  if (e != cudaSuccess || P.text_tiles_per_head == 0) return e;
+  text_combine_kernel<128><<<(unsigned)(g.H * P.text_tiles_per_head), 256, 0, st>>>(
+      P.text_part, P.text_ml, P.out, lse, g, P.text_tiles_per_head, P.text_chunks);
+  return cudaGetLastError();
+}
+
 template <int D, int BKV, int WPQ, int EMU = 0>
 cudaError_t launch_persistent(const Geometry& g, const void* q, const void* k, const void* v, void* out,
                               float* lse, const Workspace& ws, bool rectify, bool text, cudaStream_t st,
@@ -1213,6 +1602,9 @@ cudaError_t launch_attn_tc(const Geometry& g, const void* q, const void* k, cons
   static const int persist = [] { const char* e = getenv("RSA_TC_PERSIST"); return e ? atoi(e) : 1; }();
   // RSA_TC_PEMU=n: n of every 8 ex2 pairs on the FMA pipe in the persistent kernel
   static const int pemu = [] { const char* e = getenv("RSA_TC_PEMU"); return e ? atoi(e) : 0; }();
+  // the two-tile ping-pong kernel for d = B = 128 (RSA_TC_PP=0: the persistent one-tile kernel)
+  static const int pp = [] { const char* e = getenv("RSA_TC_PP"); return e ? atoi(e) : 1; }();
+  if (pp && !perm && g.d == 128 && g.B == 128) return launch_pp(g, q, k, v, out, lse, ws, rectify, text, st);
   if (persist && qtm && !vt && emu == 0) {
     if (g.d == 128 && g.B == 128 && pemu == 1)
       return launch_persistent<128, 128, 2, 1>(g, q, k, v, out, lse, ws, rectify, text, st, perm);
