@@ -80,6 +80,7 @@ struct TcParams {
   int trace_cta;     // CTA traced per step when stamps == 2
   int stamps;        // RSA_TC_STAMPS=1: per-CTA globaltimer stamps into `lse` (profiling)
   int qring;         // persistent kernel: each tile's Q rows arrive by TMA in a K/V ring stage
+  int pp_lock;       // ping-pong kernel: each MMA group + commits issued under a CTA lock
   int mma_spin;      // persistent kernel: the MMA warp polls P (no try_wait suspend)
   int sm_spin;       // persistent kernel: the softmax warps poll S
   int mode;          // 0 normal; diagnostics: 1 no softmax math, 2 TMA only, 3 MMA only, 4 MMA+TMA,
@@ -1131,6 +1132,7 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
   // per slot: q_full, q_empty, kv_full[2], kv_empty[2], s_full[2], pv_done, p_full[2], o_full  (12 barriers)
   auto slot_bar = [&](int s, int i) { return bars + s * 12 + i; };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
+  int* issue_lock = reinterpret_cast<int*>(bars + 25);   // (pp_lock) one slot's MMA group at a time
 
   const Geometry& g = P.g;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -1149,6 +1151,7 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
       ptx::mbar_init(slot_bar(s, 10), 128);  // p_full[1]
       ptx::mbar_init(slot_bar(s, 11), 1);    // o_full: the tile's last PV is complete
     }
+    *issue_lock = 0;
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc<512>(tmem_slot);
@@ -1238,6 +1241,9 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
         const uint32_t kb = ring + (uint32_t)(sj * C::STAGE) + (uint32_t)(half * 64 * 128);
         const uint32_t d_tmem = tm + (uint32_t)(half * 64);
         if (ptx::elect_one()) {
+          if (P.pp_lock)
+            while (atomicCAS(issue_lock, 0, 1) != 0) {
+            }
 #pragma unroll
           for (int k = 0; k < D / 16; ++k) {
             const uint32_t off = (uint32_t)((k / 4) * C::Q_PANEL + (k % 4) * 32);
@@ -1248,6 +1254,7 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
           if (half == 1) ptx::tc_commit(slot_bar(s, 4 + sj));   // K_j fully read
           ptx::tc_commit(slot_bar(s, 6 + half));                  // s_full[half]
           if (i == nsub - 1) ptx::tc_commit(slot_bar(s, 1));      // Q may be replaced after this
+          if (P.pp_lock) atomicExch(issue_lock, 0);
         }
         __syncwarp();
       };
@@ -1266,6 +1273,9 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
         ptx::tc_fence_after();
         const uint32_t vb = ring + (uint32_t)(sv * C::STAGE) + (uint32_t)(half * 64 * 128);
         if (ptx::elect_one()) {
+          if (P.pp_lock)
+            while (atomicCAS(issue_lock, 0, 1) != 0) {
+            }
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const uint64_t b = ptx::sw128_desc(vb + k * 2048, C::KV_PANEL, 1024);
@@ -1273,6 +1283,7 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
           }
           if (half == 1) ptx::tc_commit(slot_bar(s, 4 + sv));   // V_j fully read
           ptx::tc_commit(slot_bar(s, 8));                         // pv_done
+          if (P.pp_lock) atomicExch(issue_lock, 0);
         }
         __syncwarp();
         if (i + 2 < nsub) issue_s(i + 2);
@@ -1466,6 +1477,8 @@ cudaError_t launch_pp(const Geometry& g, const void* q, const void* k, const voi
   P.text_part = ws.text_part;
   P.text_ml = reinterpret_cast<float2*>(ws.text_ml);
   P.scale_log2 = (float)(1.4426950408889634 / sqrt((double)g.d));
+  static const int lock_env = [] { const char* e = getenv("RSA_TC_PP_LOCK"); return e ? atoi(e) : 0; }();
+  P.pp_lock = lock_env;
   cudaError_t e = cudaFuncSetAttribute(attn_tc_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
