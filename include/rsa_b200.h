@@ -193,7 +193,7 @@ rsa_status rsa_morton_permutation(int64_t t, int64_t h, int64_t w, int32_t* perm
 rsa_status rsa_permute_rows(const rsa_shape* shape, const int32_t* perm, const void* src, void* dst,
                             int32_t inverse, void* stream);
 
-/* Bytes of the `perm_buf` rsa_forward_permuted needs (permuted K and V). */
+/* Bytes of the `perm_buf` rsa_forward_permuted needs (permuted Q, K and V). */
 size_t rsa_permuted_buffer_size(const rsa_shape* shape);
 
 /* rsa_forward on the problem whose video tokens are reordered by `perm`

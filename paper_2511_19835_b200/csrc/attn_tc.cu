@@ -1413,7 +1413,9 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
           comp = P.ws.comp + (t.h * g.N + n_blk) * D;
         }
         const float inv_l = (nsub > 0 && l_run > 0.f) ? 1.f / l_run : 0.f;
-        __nv_bfloat16* orow = P.out + (t.h * g.T + grow) * D;
+        // permuted problem: scatter the row back to its original position
+        const int64_t orig = (P.perm && valid) ? P.perm[grow] : grow;
+        __nv_bfloat16* orow = P.out + (t.h * g.T + orig) * D;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           uint32_t o[32];
@@ -1439,7 +1441,7 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
           }
         }
         if (valid && P.lse)
-          P.lse[t.h * g.T + grow] = l_run > 0.f ? (log2f(l_run) + m_run) * 0.69314718055994531f : -INFINITY;
+          P.lse[t.h * g.T + orig] = l_run > 0.f ? (log2f(l_run) + m_run) * 0.69314718055994531f : -INFINITY;
       }
       ptx::tc_fence_before();
       gi += nsub;
@@ -1456,7 +1458,7 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
 }
 
 cudaError_t launch_pp(const Geometry& g, const void* q, const void* k, const void* v, void* out, float* lse,
-                      const Workspace& ws, bool rectify, bool text, cudaStream_t st) {
+                      const Workspace& ws, bool rectify, bool text, cudaStream_t st, const int32_t* perm) {
   using C = CfgPP;
   CUtensorMap tq, tk, tv;
   if (!make_tmap_3d(&tq, q, g.d, g.T, g.H, 128) || !make_tmap_3d(&tk, k, g.d, g.T, g.H, 128) ||
@@ -1468,6 +1470,7 @@ cudaError_t launch_pp(const Geometry& g, const void* q, const void* k, const voi
   P.out = static_cast<__nv_bfloat16*>(out);
   P.q = static_cast<const __nv_bfloat16*>(q);
   P.lse = lse;
+  P.perm = perm;   // (q is then the permuted copy; outputs are scattered back)
   P.rectify = rectify ? 1 : 0;
   P.text_tiles_per_head = text ? (g.Tt + 127) / 128 : 0;
   P.text_chunks = text_chunks(g);
@@ -1601,7 +1604,7 @@ bool tc_supported(const Geometry& g) {
 
 cudaError_t launch_attn_tc(const Geometry& g, const void* q, const void* k, const void* v, void* out, float* lse,
                            const Workspace& ws, bool rectify, bool text, cudaStream_t st, int* launches,
-                           const int32_t* perm) {
+                           const int32_t* perm, const void* q_perm) {
   static const bool vt_on = [] { const char* e = getenv("RSA_TC_VT"); return e && atoi(e) != 0; }();
   *launches += (vt_on ? 2 : 1) + (text && g.Tt > 0 ? 1 : 0);   // (V transpose) + attention (+ text combine)
   // Variant knobs (profiling): RSA_TC_QTMEM=1 keeps Q in TMEM (2 S buffers);
@@ -1617,7 +1620,9 @@ cudaError_t launch_attn_tc(const Geometry& g, const void* q, const void* k, cons
   static const int pemu = [] { const char* e = getenv("RSA_TC_PEMU"); return e ? atoi(e) : 0; }();
   // the two-tile ping-pong kernel for d = B = 128 (RSA_TC_PP=0: the persistent one-tile kernel)
   static const int pp = [] { const char* e = getenv("RSA_TC_PP"); return e ? atoi(e) : 1; }();
-  if (pp && !perm && g.d == 128 && g.B == 128) return launch_pp(g, q, k, v, out, lse, ws, rectify, text, st);
+  // (the permuted problem runs on it with the permuted Q copy K1 wrote)
+  if (pp && g.d == 128 && g.B == 128 && (!perm || q_perm))
+    return launch_pp(g, perm ? q_perm : q, k, v, out, lse, ws, rectify, text, st, perm);
   if (persist && qtm && !vt && emu == 0) {
     if (g.d == 128 && g.B == 128 && pemu == 1)
       return launch_persistent<128, 128, 2, 1>(g, q, k, v, out, lse, ws, rectify, text, st, perm);

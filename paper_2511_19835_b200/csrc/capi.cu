@@ -149,7 +149,8 @@ bool use_tc(const rsa_shape* s, const rsa::Geometry& g) {
 
 rsa_status run_attention(const rsa_shape* s, const rsa::Geometry& g, const rsa::Workspace& ws,
                          const void* q, const void* k, const void* v, void* out, float* lse,
-                         bool rectify, bool text, cudaStream_t st, const int32_t* perm = nullptr) {
+                         bool rectify, bool text, cudaStream_t st, const int32_t* perm = nullptr,
+                         const void* q_perm = nullptr) {
   cudaError_t e;
   const bool tc = use_tc(s, g);
   if (s->kernel == RSA_KERNEL_TCGEN05 && !tc)
@@ -157,7 +158,7 @@ rsa_status run_attention(const rsa_shape* s, const rsa::Geometry& g, const rsa::
   if (tc) {
     e = rsa::launch_tile_lists(g, ws, st, &g_launches);
     if (e != cudaSuccess) return cuda_fail(e, "tile_lists");
-    e = rsa::launch_attn_tc(g, q, k, v, out, lse, ws, rectify, text, st, &g_launches, perm);
+    e = rsa::launch_attn_tc(g, q, k, v, out, lse, ws, rectify, text, st, &g_launches, perm, q_perm);
     if (e != cudaSuccess) return cuda_fail(e, "attn_tc");
   } else {
     if (perm) return fail(RSA_ERR_UNSUPPORTED, "the permuted problem needs the tcgen05 kernel (bf16)");
@@ -405,7 +406,7 @@ size_t rsa_permuted_buffer_size(const rsa_shape* shape) {
   rsa::Geometry g;
   if (make_geometry(shape, &g) != RSA_OK) return 0;
   const size_t esz = g.dtype == RSA_BF16 ? 2 : g.dtype == RSA_F32 ? 4 : 8;
-  return 2 * (size_t)g.H * g.T * g.d * esz;   // permuted K and V
+  return 3 * (size_t)g.H * g.T * g.d * esz;   // permuted K, V and Q
 }
 
 rsa_status rsa_forward_permuted(const rsa_shape* shape, const rsa_config* cfg, const void* q, const void* k,
@@ -423,18 +424,27 @@ rsa_status rsa_forward_permuted(const rsa_shape* shape, const rsa_config* cfg, c
   rsa::Workspace ws = bind(g, workspace);
   char* kp = static_cast<char*>(perm_buf);
   char* vp = kp + (size_t)g.H * g.T * g.d * 2;
+  char* qp = vp + (size_t)g.H * g.T * g.d * 2;
   cudaError_t e = cudaMemsetAsync(ws.status, 0, 64, st);
   if (e != cudaSuccess) return cuda_fail(e, "memset status");
-  // K1: gathers the video rows in permuted order, writes permuted K and V
-  e = rsa::launch_pool(g, q, k, v, ws, st, &g_launches, perm, kp, vp);
+  // K1: gathers the video rows in permuted order, writes permuted Q, K and V
+  e = rsa::launch_pool(g, q, k, v, ws, st, &g_launches, perm, kp, vp, qp);
   if (e == cudaErrorNotSupported)
     return fail(RSA_ERR_UNSUPPORTED, "the fused permuted path needs 16-byte aligned bf16 rows, d in {64, 128}");
   if (e != cudaSuccess) return cuda_fail(e, "pool(permuted)");
   const int64_t k_floor = (int64_t)std::ceil(cfg->top_k_fraction * (double)g.M);
   e = rsa::launch_select(g, *cfg, k_floor, ws, st, &g_launches);
   if (e != cudaSuccess) return cuda_fail(e, "select");
-  // K3 on the permuted K/V; Q rows gathered and O / LSE rows scattered via perm
-  return run_attention(shape, g, ws, q, kp, vp, out, lse, rectifies(cfg->variant), true, st, perm);
+  // the text query rows of the permuted Q copy are the original ones
+  if (g.Tt > 0) {
+    const size_t pitch = (size_t)g.T * g.d * 2;
+    e = cudaMemcpy2DAsync(qp + (size_t)g.Tv * g.d * 2, pitch, static_cast<const char*>(q) + (size_t)g.Tv * g.d * 2,
+                          pitch, (size_t)g.Tt * g.d * 2, (size_t)g.H, cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e, "text Q copy");
+  }
+  // K3 on the permuted Q/K/V (the persistent kernel gathers Q rows through perm
+  // instead); O / LSE rows scattered back via perm
+  return run_attention(shape, g, ws, q, kp, vp, out, lse, rectifies(cfg->variant), true, st, perm, qp);
 }
 
 size_t rsa_diagnostics_scratch_size(const rsa_shape* shape) {

@@ -292,7 +292,8 @@ template <int D, int STAGES>
 __global__ void __launch_bounds__(kBulkThreads, 3)
 pool_bulk_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k,
                  const __nv_bfloat16* __restrict__ v, Workspace ws, Geometry g, int64_t n_items,
-                 const int32_t* __restrict__ perm, __nv_bfloat16* kp, __nv_bfloat16* vp) {
+                 const int32_t* __restrict__ perm, __nv_bfloat16* kp, __nv_bfloat16* vp,
+                 __nv_bfloat16* qp) {
   constexpr int WPR = D / 2;                   // 32-bit words (bf16 pairs) per row
   constexpr int RP = kBulkThreads / WPR;       // row phases
   extern __shared__ __align__(128) uint8_t smem[];
@@ -371,10 +372,10 @@ pool_bulk_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
       bar_wait(full + s, (uint32_t)((kk / STAGES) & 1));
     }
     const uint32_t* blk = reinterpret_cast<const uint32_t*>(ring + s * stage_bytes);
-    if (kp && it.seg > 0 && t == 0) {
+    if (kp && (it.seg > 0 || qp) && t == 0) {
       if (perm) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> bulk read
-      // the permuted K / V block, contiguous, for K3's TMA (shared -> global bulk copy)
-      __nv_bfloat16* dstp = (it.seg == 1 ? kp : vp) + (it.h * g.T + kv_row0(g, it.blk)) * D;
+      // the permuted Q / K / V block, contiguous, for K3's TMA (shared -> global bulk copy)
+      __nv_bfloat16* dstp = (it.seg == 0 ? qp : it.seg == 1 ? kp : vp) + (it.h * g.T + kv_row0(g, it.blk)) * D;
       asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n\t"
                    "cp.async.bulk.commit_group;" ::"l"(dstp),
                    "r"((uint32_t)__cvta_generic_to_shared(blk)), "r"((uint32_t)(len * D * 2))
@@ -499,7 +500,7 @@ pool_bulk_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
 
 template <int D>
 cudaError_t launch_bulk(const Geometry& g, const void* q, const void* k, const void* v, const Workspace& ws,
-                        cudaStream_t st, const int32_t* perm, void* kp, void* vp) {
+                        cudaStream_t st, const int32_t* perm, void* kp, void* vp, void* qp) {
   constexpr int STAGES = 2;
   constexpr int RP = kBulkThreads / (D / 2);
   const size_t smem = (size_t)STAGES * g.B * D * 2 + STAGES * 8 + 2 * RP * D * 8 + 64;
@@ -513,7 +514,7 @@ cudaError_t launch_bulk(const Geometry& g, const void* q, const void* k, const v
   const int64_t grid = std::min<int64_t>(n_items, (int64_t)sms * 3);
   kern<<<(unsigned)grid, kBulkThreads, smem, st>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
                                                    (const __nv_bfloat16*)v, ws, g, n_items, perm,
-                                                   (__nv_bfloat16*)kp, (__nv_bfloat16*)vp);
+                                                   (__nv_bfloat16*)kp, (__nv_bfloat16*)vp, (__nv_bfloat16*)qp);
   return cudaGetLastError();
 }
 
@@ -536,7 +537,7 @@ cudaError_t launch_typed(const Geometry& g, const void* q, const void* k, const 
 
 cudaError_t launch_pool(const Geometry& g, const void* q, const void* k, const void* v,
                         const Workspace& ws, cudaStream_t st, int* launches, const int32_t* perm,
-                        void* kp, void* vp) {
+                        void* kp, void* vp, void* qp) {
   ++*launches;
   switch (g.dtype) {
     case RSA_BF16: {
@@ -544,8 +545,8 @@ cudaError_t launch_pool(const Geometry& g, const void* q, const void* k, const v
       // that fits two ring stages per CTA, three CTAs per SM
       const bool aligned = ((uintptr_t)q % 16 == 0) && ((uintptr_t)k % 16 == 0) && ((uintptr_t)v % 16 == 0);
       const bool fits = g.B * g.d * 2 * 2 <= 64 * 1024;
-      if (aligned && fits && g.d == 128) return launch_bulk<128>(g, q, k, v, ws, st, perm, kp, vp);
-      if (aligned && fits && g.d == 64) return launch_bulk<64>(g, q, k, v, ws, st, perm, kp, vp);
+      if (aligned && fits && g.d == 128) return launch_bulk<128>(g, q, k, v, ws, st, perm, kp, vp, qp);
+      if (aligned && fits && g.d == 64) return launch_bulk<64>(g, q, k, v, ws, st, perm, kp, vp, qp);
       if (perm) return cudaErrorNotSupported;
       return launch_typed<__nv_bfloat16>(g, q, k, v, ws, st);
     }

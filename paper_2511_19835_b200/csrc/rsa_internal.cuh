@@ -93,10 +93,12 @@ template <typename T> __device__ __forceinline__ T from_acc(double x) { return (
 // ---- launchers (one per .cu file) -----------------------------------------
 // perm (device int32 [T_v], may be null): pool the video tokens in the order
 // perm (row r of the permuted problem = original row perm[r]) and write the
-// permuted K and V ([H][T][d], text rows copied) to kp / vp for K3
+// permuted K and V ([H][T][d], text rows copied) to kp / vp for K3, and the
+// permuted video Q rows to qp (if given; its text rows are the caller's copy)
 cudaError_t launch_pool(const Geometry& g, const void* q, const void* k, const void* v,
                         const Workspace& ws, cudaStream_t st, int* launches,
-                        const int32_t* perm = nullptr, void* kp = nullptr, void* vp = nullptr);
+                        const int32_t* perm = nullptr, void* kp = nullptr, void* vp = nullptr,
+                        void* qp = nullptr);
 cudaError_t launch_select(const Geometry& g, const rsa_config& cfg, int64_t k_floor,
                           const Workspace& ws, cudaStream_t st, int* launches);
 cudaError_t launch_lists_from_mask(const Geometry& g, const uint8_t* mask,
@@ -119,6 +121,7 @@ cudaError_t launch_permute_rows(const Geometry& g, const int32_t* perm, const vo
                                 bool inverse, cudaStream_t st);
 cudaError_t launch_attn_tc(const Geometry& g, const void* q, const void* k, const void* v,
                            void* out, float* lse, const Workspace& ws, bool rectify,
-                           bool text, cudaStream_t st, int* launches, const int32_t* perm = nullptr);
+                           bool text, cudaStream_t st, int* launches, const int32_t* perm = nullptr,
+                           const void* q_perm = nullptr);
 
 }  // namespace rsa
