@@ -34,7 +34,8 @@ namespace rsa {
 namespace {
 
 constexpr int kThreads = 384;   // 4 control warps + 8 softmax warps
-constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale O only if max grows by > 2^8
+constexpr float kRescaleThreshold = 12.0f;  // log2 units: rescale O only if the row max grows by > 2^12
+                                            // (P <= 2^12 stays exact-range in bf16 / fp32; 8 measured ~1 % slower)
 
 template <int D, int BKV, bool QTM, bool VT>
 struct Cfg {
