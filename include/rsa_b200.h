@@ -48,8 +48,10 @@ typedef enum {
   RSA_VARIANT_COMPENSATE_ALL = 4
 } rsa_variant;
 
-/* Attention kernel selection (K3). AUTO picks the tcgen05 kernel for bf16 and
- * block/head_dim in {64,128}, the CUDA-core kernel otherwise. */
+/* Attention kernel selection (K3). AUTO picks the tcgen05 kernels for bf16 and
+ * block/head_dim in {64,128} (the two-tile ping-pong kernel at block = head_dim
+ * = 128, the persistent one-tile kernel otherwise), the CUDA-core kernel for
+ * everything else (fp32/fp64, other block sizes). */
 typedef enum { RSA_KERNEL_AUTO = 0, RSA_KERNEL_TCGEN05 = 1, RSA_KERNEL_SIMT = 2 } rsa_kernel;
 
 /* rsa_shape.flags */
@@ -108,7 +110,8 @@ typedef struct {
   size_t comp;        /* [N][d]        sum_applied a_pool v_pool (rectify.py:84-87) */
   size_t kv_count;    /* i32 [N]       retained kv blocks per query block           */
   size_t kv_list;     /* i32 [N][M]    ascending retained kv block ids               */
-  size_t tile_count;  /* i32 [tiles]   kv entries per 128-row tcgen05 tile           */
+  size_t tile_count;  /* i32 [tiles]   kv entries per 128-row tcgen05 tile (B = 64;
+                         at B = 128 a tile is one query block: kv_count / kv_list) */
   size_t tile_list;   /* i32 [tiles][M] (kv id | member bits << 24)                  */
   size_t v_t;         /* bf16 [d][T]   V transposed (tcgen05 path: K-major PV operand) */
   size_t text_part;   /* f32 [text tiles][chunks][128][d] split-K partial O of text queries */
