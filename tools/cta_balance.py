@@ -8,6 +8,7 @@ import numpy as np
 import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+os.environ.setdefault("RSA_TC_PP", "0")   # the stamps are implemented in the persistent / one-tile kernels
 os.environ["RSA_TC_STAMPS"] = "4"
 import bench  # noqa: E402
 from paper_2511_19835_b200 import _native as nat  # noqa: E402

@@ -9,6 +9,7 @@ import numpy as np
 import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+os.environ.setdefault("RSA_TC_PP", "0")   # the stamps are implemented in the persistent / one-tile kernels
 os.environ["RSA_TC_STAMPS"] = "3"
 os.environ.setdefault("RSA_TC_TRACE_CTA", "7")
 import bench  # noqa: E402
