@@ -22,7 +22,9 @@ CSRC = PKG / "csrc"
 OBJ = PKG / "_build"
 LIB = PKG / "librsa_b200.so"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVCC_FLAGS = ["-O3", *os.environ.get("RSA_EXTRA_NVCC", "").split(),   # (extra -D flags for A/B builds) "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+# RSA_EXTRA_NVCC: extra -D flags for A/B builds
+NVCC_FLAGS = ["-O3", *os.environ.get("RSA_EXTRA_NVCC", "").split(), "-std=c++17", "-lineinfo", "-Xcompiler",
+              "-fPIC", "--expt-relaxed-constexpr",
               "-Xptxas", "-v", "-I", str(ROOT / "include")]
 
 
