@@ -1171,6 +1171,7 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
       ptx::prefetch_tmap(&tm_k);
       ptx::prefetch_tmap(&tm_v);
       const uint64_t keep = ptx::policy_evict_last();
+      const uint64_t once = ptx::policy_evict_first();
       uint8_t* qs = base + s * C::SLOT_SMEM;
       uint8_t* ring = qs + C::Q_BYTES;
       int st = 0;
@@ -1182,7 +1183,8 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
         ptx::mbar_expect_tx(slot_bar(s, 0), C::Q_BYTES);
 #pragma unroll
         for (int p = 0; p < 2; ++p)
-          ptx::tma_load_3d(qs + p * C::Q_PANEL, &tm_q, slot_bar(s, 0), 64 * p, (int)t.q_row0, (int)t.h);
+          ptx::tma_load_3d_hint(qs + p * C::Q_PANEL, &tm_q, slot_bar(s, 0), 64 * p, (int)t.q_row0, (int)t.h,
+                                once);   // Q rows are read by one tile: keep L2 for K/V
         for (int64_t j = 0; j < t.count; ++j) {
           const int64_t m = t.list ? (t.list[j] & 0xFFFFFF) : t.m_first + j;
 #pragma unroll
