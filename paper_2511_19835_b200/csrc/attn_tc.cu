@@ -1313,11 +1313,19 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
       const TileDesc t = decode_tile(P, bid);
       const int64_t count = t.count, nsub = 2 * count;
       float m_run = -INFINITY, l_run = 0.f;
+      // the kv list entry (for the ragged-block masks) is fetched one block ahead:
+      // a global load per sub-step sat on the softmax critical path
+      int32_t ent_next = (t.list && count > 0) ? t.list[0] : 0;
+      int blen = 0;
       for (int64_t i = 0; i < nsub; ++i) {
         const int64_t gsub = gi + i;
         const int half = (int)(i & 1);
-        const int64_t m = t.list ? (t.list[i >> 1] & 0xFFFFFF) : t.m_first + (i >> 1);
-        const int blen = (int)kv_len(g, m);
+        if (half == 0) {
+          const int64_t jb = i >> 1;
+          const int64_t m = t.list ? (ent_next & 0xFFFFFF) : t.m_first + jb;
+          if (t.list && jb + 1 < count) ent_next = t.list[jb + 1];
+          blen = (int)kv_len(g, m);
+        }
         const int len = blen - half * 64;
         ptx::mbar_wait(slot_bar(s, 6 + half), (uint32_t)((gsub >> 1) & 1));
         ptx::tc_fence_after();
