@@ -1116,7 +1116,7 @@ struct CfgPP {
   static constexpr int Q_PANEL = 128 * 128;
   static constexpr int Q_BYTES = 128 * D * 2;     // 32 KB
   static constexpr int SLOT_SMEM = Q_BYTES + NST * STAGE;
-  static constexpr int SMEM = 1024 + 2 * SLOT_SMEM + 512;
+  static constexpr int SMEM = 1024 + 2 * SLOT_SMEM + 512 + 2 * 2 * 128 * 4;   // + parked compensation rows
   static constexpr uint32_t IDESC_S64 = ptx::idesc_bf16(128, 64, false);   // S sub-steps: 64 keys
   static constexpr uint32_t IDESC_O = ptx::idesc_bf16(128, D, true);   // V MN-major
   static constexpr int THREADS = 384;
@@ -1134,6 +1134,7 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
   auto slot_bar = [&](int s, int i) { return bars + s * 12 + i; };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
   int* issue_lock = reinterpret_cast<int*>(bars + 25);   // (pp_lock) one slot's MMA group at a time
+  float* comp_s = reinterpret_cast<float*>(bars + 64);   // [slot][tile parity][D] compensation rows
 
   const Geometry& g = P.g;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -1313,6 +1314,16 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
       const TileDesc t = decode_tile(P, bid);
       const int64_t count = t.count, nsub = 2 * count;
       float m_run = -INFINITY, l_run = 0.f;
+      // this tile's compensation row and factor (one query block per tile at
+      // B = 128): fetched now, parked in shared memory (double-buffered by tile
+      // parity), read by the epilogue after the slot's barrier
+      float rpre = 1.f;
+      float* comp_park = comp_s + (s * 2 + (int)(tix_s & 1)) * D;
+      if (P.rectify && !t.text) {
+        const int64_t n_blk = t.q_row0 / g.B;
+        comp_park[row] = (float)P.ws.comp[(t.h * g.N + n_blk) * D + row];
+        rpre = P.ws.r_eff[t.h * g.N + n_blk];
+      }
       // the kv list entry (for the ragged-block masks) is fetched one block ahead:
       // a global load per sub-step sat on the softmax critical path
       int32_t ent_next = (t.list && count > 0) ? t.list[0] : 0;
@@ -1398,6 +1409,7 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
       ptx::mbar_wait(slot_bar(s, 11), (uint32_t)(tix_s & 1));
       ptx::tc_fence_after();
       ++tix_s;
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + s) : "memory");   // the slot's parked compensation row
       const bool valid = row < t.rows_valid;
       const int64_t grow = t.q_row0 + row;
       if (t.text) {
@@ -1416,13 +1428,8 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
         }
         if (valid) P.text_ml[t.part * 128 + row] = make_float2(m_run, l_run);
       } else {
-        float rfac = 1.f;
-        const double* comp = nullptr;
-        if (P.rectify && valid) {
-          const int64_t n_blk = grow / g.B;
-          rfac = P.ws.r_eff[t.h * g.N + n_blk];
-          comp = P.ws.comp + (t.h * g.N + n_blk) * D;
-        }
+        const float rfac = (P.rectify && valid) ? rpre : 1.f;
+        const float* comp = (P.rectify && valid) ? comp_park : nullptr;
         const float inv_l = (nsub > 0 && l_run > 0.f) ? 1.f / l_run : 0.f;
         // permuted problem: scatter the row back to its original position
         const int64_t orig = (P.perm && valid) ? P.perm[grow] : grow;
