@@ -163,7 +163,84 @@ void run_step(const char* name) {
   cudaFree(d);
 }
 
+
+// The ping-pong kernel's per-block MMA sequence for one slot: two S halves as SS
+// MMAs (A = Q in shared memory, 128 x 128; B = 64 keys, N = 64) + commits, then
+// two PV halves (TS, A = P in TMEM, B = V MN-major, K = 64 keys each) + commits.
+// `slots` = 2 runs two such streams from two warps into disjoint TMEM columns.
+template <int SLOTS>
+__global__ void __launch_bounds__(128, 1) pp_bench(long long* out, int steps) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint32_t slot;
+  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ __align__(8) uint64_t dummy[8];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x / 32;
+  if (threadIdx.x == 0) { mbar_init(bar, 1); mbar_init(bar + 1, 1); for (int i = 0; i < 8; ++i) mbar_init(dummy + i, 1); fence_barrier_init(); }
+  if (warp == 0) tmem_alloc<512>(&slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  constexpr uint32_t IDS = idesc_bf16(128, 64, false);
+  constexpr uint32_t IDO = idesc_bf16(128, 128, true);
+  if (warp >= 1 && warp <= SLOTS) {
+    const int s = warp - 1;
+    const uint32_t qa = __shfl_sync(0xffffffffu, smem_u32(base + s * 98304), 0);
+    const uint32_t kb = qa + 32768, vb = qa + 65536;
+    const uint32_t tm = tmem + (uint32_t)(s * 256);
+    long long t0 = clock64();
+    for (int j = 0; j < steps; ++j) {
+      if (elect_one()) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            mma_ss(tm + h * 64, sw128_desc(qa + (k / 4) * 16384 + (k % 4) * 32, 16, 1024),
+                   sw128_desc(kb + h * 8192 + (k / 4) * 16384 + (k % 4) * 32, 16, 1024), IDS, k > 0);
+          tc_commit(dummy + 4 * s + h);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            mma_ts(tm + 128, tm + h * 64 + k * 8, sw128_desc(vb + h * 8192 + k * 2048, 16384, 1024), IDO, 1);
+          tc_commit(dummy + 4 * s + 2 + h);
+        }
+      }
+      __syncwarp();
+    }
+    if (elect_one()) tc_commit(bar + s);
+    __syncwarp();
+    mbar_wait(bar + s, 0);
+    if ((threadIdx.x & 31) == 0) out[blockIdx.x * 2 + s] = clock64() - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) { tc_fence_after(); tmem_dealloc<512>(tmem); }
+}
+
+template <int SLOTS>
+void run_pp(const char* name) {
+  long long* d;
+  const int sms = 148, steps = 2048;
+  cudaMalloc(&d, 2 * sms * sizeof(long long));
+  auto k = pp_bench<SLOTS>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  k<<<sms, 128, 200 * 1024>>>(d, steps);
+  k<<<sms, 128, 200 * 1024>>>(d, steps);
+  long long h[296];
+  cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  double avg = 0;
+  for (int i = 0; i < sms; ++i) avg += h[2 * i];
+  printf("%-34s cycles/block/slot %7.1f (ideal %d)  err=%s\n", name, avg / sms / steps, 1024 * SLOTS,
+         cudaGetErrorString(cudaGetLastError()));
+  cudaFree(d);
+}
+
 int main() {
+  run_pp<1>("ping-pong block, 1 slot");
+  run_pp<2>("ping-pong block, 2 slots");
   run_step<false, true>("kernel step: V MN-major + commits");
   run_step<true, true>("kernel step: V^T K-major + commits");
   run_step<false, false>("kernel step: V MN-major, no commits");
