@@ -237,6 +237,15 @@ rsa_status rsa_dense_reference(const rsa_shape* shape, const void* q, const void
  * reallocation denominator <= 0, ipar.py:62-64) into an rsa_status. */
 rsa_status rsa_check_device_status(void* workspace, void* stream);
 
+/* Stream-ordered, non-synchronising status: ORs the call's device status
+ * flags (int32[4]: degenerate row, empty row, deficit, non-finite input)
+ * into the caller's device buffer `status_accum`, which the caller zeroes
+ * once and may read back whenever it synchronises anyway (a model loop).
+ * rsa_status_from_flags() turns a host copy of those flags into the status
+ * rsa_check_device_status() would have returned. */
+rsa_status rsa_accumulate_status(const void* workspace, int32_t* status_accum, void* stream);
+rsa_status rsa_status_from_flags(const int32_t* host_flags);
+
 /* Number of kernel launches the last rsa_forward/rsa_attention enqueued. */
 int32_t rsa_last_launch_count(void);
 const char* rsa_last_error(void);

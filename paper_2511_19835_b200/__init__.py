@@ -19,7 +19,7 @@ from .errors import (BlockSizeError, ConfigError, DegenerateRowError, EmptyRowEr
 __version__ = "0.1.0"
 
 _LAZY = {"rectified_attention_pipeline", "block_sparse_attention", "text_full_attention",
-         "rectified_sparse_attention"}
+         "rectified_sparse_attention", "new_status", "raise_for_status"}
 _REORDER = {"morton_permutation", "reorder_morton", "inverse_permutation"}
 _DIAG = {"gain_error", "gapr_condition_agreement", "denominator_equivalence_report"}
 _HARNESS = {"run_variants", "full_attention_reference", "normalized_l1", "cosine_similarity", "AlignmentReport"}

@@ -25,7 +25,8 @@ EXPORTS = ("rsa_plan", "rsa_workspace_layout_query", "rsa_workspace_size", "rsa_
            "rsa_text_full_attention", "rsa_morton_permutation", "rsa_permute_rows",
            "rsa_permuted_buffer_size", "rsa_forward_permuted", "rsa_diagnostics_scratch_size", "rsa_diagnostics",
            "rsa_dense_reference_scratch_size", "rsa_dense_reference",
-           "rsa_check_device_status", "rsa_last_launch_count",
+           "rsa_check_device_status", "rsa_accumulate_status", "rsa_status_from_flags",
+           "rsa_last_launch_count",
            "rsa_last_error", "rsa_version")
 
 
@@ -97,6 +98,8 @@ def lib() -> C.CDLL:
         "rsa_dense_reference_scratch_size": ([C.POINTER(Shape)], C.c_size_t),
         "rsa_dense_reference": ([C.POINTER(Shape), P, P, P, P, P, P], C.c_int),
         "rsa_check_device_status": ([P, P], C.c_int),
+        "rsa_accumulate_status": ([P, P, P], C.c_int),
+        "rsa_status_from_flags": ([P], C.c_int),
         "rsa_last_launch_count": ([], C.c_int32),
         "rsa_last_error": ([], C.c_char_p),
         "rsa_version": ([], C.c_char_p),

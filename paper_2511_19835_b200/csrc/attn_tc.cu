@@ -1264,6 +1264,13 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
       };
       if (nsub > 0) issue_s(0);
       if (nsub > 1) issue_s(1);
+      // a tile with an empty kv list (the C ABI's mask seam flags it as
+      // RSA_ERR_EMPTY_ROW) issues no S MMA: release its Q buffer here, or the
+      // producer would wait for it forever
+      if (nsub == 0) {
+        if (ptx::elect_one()) ptx::tc_commit(slot_bar(s, 1));
+        __syncwarp();
+      }
       for (int64_t i = 0; i < nsub; ++i) {
         const int64_t gsub = gi + i;
         const int64_t j = i >> 1;

@@ -153,8 +153,13 @@ rsa_status run_attention(const rsa_shape* s, const rsa::Geometry& g, const rsa::
                          const void* q_perm = nullptr) {
   cudaError_t e;
   const bool tc = use_tc(s, g);
-  if (s->kernel == RSA_KERNEL_TCGEN05 && !tc)
-    return fail(RSA_ERR_UNSUPPORTED, "tcgen05 kernel needs bf16 and block, head_dim in {64, 128}");
+  // bf16 runs on the tensor-core kernel; the CUDA-core kernel serves the
+  // reference's fp32/fp64 precisions, and bf16 only when asked for by name
+  // (a cross-check) -- never as a silent second backend
+  if ((s->kernel == RSA_KERNEL_TCGEN05 || (s->kernel == RSA_KERNEL_AUTO && g.dtype == RSA_BF16)) && !tc)
+    return fail(RSA_ERR_UNSUPPORTED, "bf16 attention runs on the tcgen05 kernel, which needs block and "
+                                     "head_dim in {64, 128} (kernel='simt' selects the CUDA-core kernel "
+                                     "explicitly)");
   if (tc) {
     e = rsa::launch_tile_lists(g, ws, st, &g_launches);
     if (e != cudaSuccess) return cuda_fail(e, "tile_lists");
@@ -170,6 +175,10 @@ rsa_status run_attention(const rsa_shape* s, const rsa::Geometry& g, const rsa::
     }
   }
   return RSA_OK;
+}
+
+__global__ void accumulate_status_kernel(const int32_t* __restrict__ flags, int32_t* __restrict__ accum) {
+  if (threadIdx.x < 4 && flags[threadIdx.x]) atomicOr(accum + threadIdx.x, flags[threadIdx.x]);
 }
 
 bool rectifies(int variant) {
@@ -214,19 +223,36 @@ size_t rsa_workspace_size(const rsa_shape* shape) {
   return L.total;
 }
 
-rsa_status rsa_pool(const rsa_shape* shape, const void* q, const void* k, const void* v,
-                    void* workspace, void* stream) {
+}  // extern "C"
+
+namespace {
+// K1; `reset_status` clears the device status flags first (a new call).  The
+// host-memory call keeps them across its head chunks, so an error raised by
+// any chunk survives to the final check.
+rsa_status pool_impl(const rsa_shape* shape, const void* q, const void* k, const void* v, void* workspace,
+                     void* stream, bool reset_status) {
   rsa::Geometry g;
   rsa_status s = make_geometry(shape, &g);
   if (s != RSA_OK) return s;
   if (!q || !k || !v || !workspace) return fail(RSA_ERR_SHAPE, "null pointer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   rsa::Workspace ws = bind(g, workspace);
-  cudaError_t e = cudaMemsetAsync(ws.status, 0, 64, st);
+  cudaError_t e = reset_status ? cudaMemsetAsync(ws.status, 0, 64, st) : cudaSuccess;
   if (e != cudaSuccess) return cuda_fail(e, "memset status");
   e = rsa::launch_pool(g, q, k, v, ws, st, &g_launches);
   if (e != cudaSuccess) return cuda_fail(e, "pool");
   return RSA_OK;
+}
+
+rsa_status forward_impl(const rsa_shape* shape, const rsa_config* cfg, const void* q, const void* k,
+                        const void* v, void* out, float* lse, void* workspace, void* stream, bool reset_status);
+}  // namespace
+
+extern "C" {
+
+rsa_status rsa_pool(const rsa_shape* shape, const void* q, const void* k, const void* v,
+                    void* workspace, void* stream) {
+  return pool_impl(shape, q, k, v, workspace, stream, true);
 }
 
 rsa_status rsa_select(const rsa_shape* shape, const rsa_config* cfg, void* workspace, void* stream) {
@@ -261,12 +287,44 @@ rsa_status rsa_attention(const rsa_shape* shape, const rsa_config* cfg, const vo
 rsa_status rsa_forward(const rsa_shape* shape, const rsa_config* cfg, const void* q, const void* k,
                        const void* v, void* out, float* lse, void* workspace, void* stream) {
   g_launches = 0;
-  rsa_status s = rsa_pool(shape, q, k, v, workspace, stream);
+  return forward_impl(shape, cfg, q, k, v, out, lse, workspace, stream, true);
+}
+
+}  // extern "C"
+
+namespace {
+rsa_status forward_impl(const rsa_shape* shape, const rsa_config* cfg, const void* q, const void* k,
+                        const void* v, void* out, float* lse, void* workspace, void* stream, bool reset_status) {
+  rsa_status s = pool_impl(shape, q, k, v, workspace, stream, reset_status);
   if (s != RSA_OK) return s;
   s = rsa_select(shape, cfg, workspace, stream);
   if (s != RSA_OK) return s;
   return rsa_attention(shape, cfg, q, k, v, out, lse, workspace, stream);
 }
+
+// per-thread pool of timing-free events for the host-memory call (no
+// create/destroy per call)
+cudaError_t host_events(size_t n, std::vector<cudaEvent_t>** out) {
+  static thread_local std::vector<cudaEvent_t> pool;
+  static thread_local int pool_dev = -1;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (pool_dev != dev) {   // events belong to a device: start a fresh pool (old ones are leaked, not reused)
+    pool.clear();
+    pool_dev = dev;
+  }
+  while (pool.size() < n) {
+    cudaEvent_t x;
+    if ((e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming)) != cudaSuccess) return e;
+    pool.push_back(x);
+  }
+  *out = &pool;
+  return cudaSuccess;
+}
+}  // namespace
+
+extern "C" {
 
 // End-to-end call from host memory: heads are processed in chunks so chunk
 // c+1's host->device copy (copy-in stream) overlaps chunk c's K1->K2->K3
@@ -298,9 +356,9 @@ rsa_status rsa_forward_host(const rsa_shape* shape, const rsa_config* cfg, const
   const size_t esz = g.dtype == RSA_BF16 ? 2 : g.dtype == RSA_F32 ? 4 : 8;
   const size_t head_bytes = (size_t)g.T * g.d * esz;
   const int64_t n_chunks = (g.H + heads_per_chunk - 1) / heads_per_chunk;
-  std::vector<cudaEvent_t> ev(3 * n_chunks + 1);
-  for (auto& x : ev)
-    if ((e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(e, "event");
+  std::vector<cudaEvent_t>* evp = nullptr;
+  if ((e = host_events((size_t)(3 * n_chunks + 1), &evp)) != cudaSuccess) return cuda_fail(e, "event");
+  std::vector<cudaEvent_t>& ev = *evp;
   // the copy-in stream starts after whatever the caller queued on `stream`
   cudaEventRecord(ev[3 * n_chunks], st);
   cudaStreamWaitEvent(s_in, ev[3 * n_chunks], 0);
@@ -310,15 +368,19 @@ rsa_status rsa_forward_host(const rsa_shape* shape, const rsa_config* cfg, const
     const size_t off = (size_t)h0 * head_bytes, bytes = (size_t)hc * head_bytes;
     auto H = [&](const void* p) { return static_cast<const char*>(p) + off; };
     auto D = [&](void* p) { return static_cast<char*>(p) + off; };
-    cudaMemcpyAsync(D(dq), H(host_q), bytes, cudaMemcpyHostToDevice, s_in);
-    cudaMemcpyAsync(D(dk), H(host_k), bytes, cudaMemcpyHostToDevice, s_in);
-    if ((e = cudaMemcpyAsync(D(dv), H(host_v), bytes, cudaMemcpyHostToDevice, s_in)) != cudaSuccess)
+    if ((e = cudaMemcpyAsync(D(dq), H(host_q), bytes, cudaMemcpyHostToDevice, s_in)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(D(dk), H(host_k), bytes, cudaMemcpyHostToDevice, s_in)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(D(dv), H(host_v), bytes, cudaMemcpyHostToDevice, s_in)) != cudaSuccess)
       return cuda_fail(e, "H2D");
     cudaEventRecord(ev[3 * c], s_in);
     cudaStreamWaitEvent(st, ev[3 * c], 0);
     rsa_shape sub = *shape;
     sub.heads = hc;
-    s = rsa_forward(&sub, cfg, D(dq), D(dk), D(dv), D(dout), lse ? lse + h0 * g.T : nullptr, workspace, stream);
+    // the status flags are cleared by the first chunk only: a non-finite input,
+    // degenerate or empty row in any chunk survives to rsa_check_device_status
+    g_launches = 0;
+    s = forward_impl(&sub, cfg, D(dq), D(dk), D(dv), D(dout), lse ? lse + h0 * g.T : nullptr, workspace, stream,
+                     c == 0);
     launches += g_launches;
     cudaEventRecord(ev[3 * c + 1], st);
     cudaStreamWaitEvent(s_out, ev[3 * c + 1], 0);
@@ -329,7 +391,6 @@ rsa_status rsa_forward_host(const rsa_shape* shape, const rsa_config* cfg, const
   }
   // the caller's stream resumes once every output chunk is in host memory
   for (int64_t c = 0; c < n_chunks; ++c) cudaStreamWaitEvent(st, ev[3 * c + 2], 0);
-  for (auto& x : ev) cudaEventDestroy(x);
   g_launches = launches;
   if (s != RSA_OK) return s;
   e = cudaGetLastError();
@@ -490,11 +551,25 @@ rsa_status rsa_dense_reference(const rsa_shape* shape, const void* q, const void
 }
 
 rsa_status rsa_check_device_status(void* workspace, void* stream) {
+  if (!workspace) return fail(RSA_ERR_SHAPE, "null workspace");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int32_t flags[4] = {0, 0, 0, 0};
   cudaError_t e = cudaMemcpyAsync(flags, workspace, sizeof(flags), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "status readback");
+  return rsa_status_from_flags(flags);
+}
+
+rsa_status rsa_accumulate_status(const void* workspace, int32_t* status_accum, void* stream) {
+  if (!workspace || !status_accum) return fail(RSA_ERR_SHAPE, "null pointer");
+  accumulate_status_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const int32_t*>(workspace), status_accum);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? RSA_OK : cuda_fail(e, "accumulate_status");
+}
+
+rsa_status rsa_status_from_flags(const int32_t* flags) {
+  if (!flags) return fail(RSA_ERR_SHAPE, "null pointer");
   if (flags[rsa::ST_NONFINITE]) return fail(RSA_ERR_SHAPE, "q/k/v contain non-finite entries");
   if (flags[rsa::ST_DEGENERATE])
     return fail(RSA_ERR_DEGENERATE_ROW, "reallocation denominator is zero on some rows");

@@ -213,7 +213,8 @@ pool_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restric
     }
     const double flen = (double)len;
     const double mean = sum / flen;           // core.py:172 fsum(...) / length
-    const double deficit = sum - flen * mean; // masks.py:166 / masks.py:171
+    // numpy rounds the product first (no FMA contraction): masks.py:166 / masks.py:171
+    const double deficit = __dsub_rn(sum, __dmul_rn(flen, mean));
     if (seg == 0) {
       ws.q_pool[(h * g.N + blk) * d + col] = mean;
       ws.q_def[(h * g.N + blk) * d + col] = deficit;
@@ -480,7 +481,8 @@ pool_bulk_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
       }
       const double flen = (double)len;
       const double mean = sum / flen;            // core.py:172 fsum(...) / length
-      const double deficit = sum - flen * mean;  // masks.py:166 / masks.py:171
+      // numpy rounds the product first (no FMA contraction): masks.py:166 / masks.py:171
+      const double deficit = __dsub_rn(sum, __dmul_rn(flen, mean));
       if (it.seg == 0) {
         ws.q_pool[(it.h * g.N + it.blk) * D + col] = mean;
         ws.q_def[(it.h * g.N + it.blk) * D + col] = deficit;

@@ -30,3 +30,26 @@ def rectified_sparse_attention_op(q: torch.Tensor, k: torch.Tensor, v: torch.Ten
 def _(q, k, v, num_text_tokens, block, top_k_fraction, weight_threshold, adjacency_radius,
       force_text_blocks, variant):
     return torch.empty_like(q)
+
+
+@torch.library.custom_op(f"{_LIB_NS}::rectified_sparse_attention_status", mutates_args=())
+def rectified_sparse_attention_status_op(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
+                                         num_text_tokens: int, block: int, top_k_fraction: float,
+                                         weight_threshold: float, adjacency_radius: int,
+                                         force_text_blocks: bool, variant: str
+                                         ) -> tuple[torch.Tensor, torch.Tensor]:
+    """Non-synchronising form: returns (out, status int32[4]) with the device
+    flags of this call; ``raise_for_status(status)`` raises the reference
+    exception when the caller next synchronises."""
+    from .pipeline import new_status
+    status = new_status(q.device)
+    out = _impl(q, k, v, num_text_tokens=num_text_tokens, block=block, top_k_fraction=top_k_fraction,
+                weight_threshold=weight_threshold, adjacency_radius=adjacency_radius,
+                force_text_blocks=force_text_blocks, variant=variant, check_status=False, status=status)
+    return out, status
+
+
+@rectified_sparse_attention_status_op.register_fake
+def _(q, k, v, num_text_tokens, block, top_k_fraction, weight_threshold, adjacency_radius,
+      force_text_blocks, variant):
+    return torch.empty_like(q), q.new_empty(4, dtype=torch.int32)

@@ -37,6 +37,17 @@ def _as_tensor(x, device) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(x)).to(device)
 
 
+def _promote(device, *xs) -> list:
+    """Device copies of q/k/v in their common dtype -- numpy's promotion of
+    mixed-precision operands in kernel.py (float32 with float64 computes in
+    float64); the kernels read all three buffers in one dtype."""
+    ts = [_as_tensor(x, device) for x in xs]
+    dt = ts[0].dtype
+    for t in ts[1:]:
+        dt = torch.promote_types(dt, t.dtype)
+    return [t.to(dt).contiguous() for t in ts]
+
+
 def _ptr(t: torch.Tensor | None):
     return C.c_void_p(t.data_ptr()) if t is not None else None
 
@@ -50,6 +61,30 @@ def workspace_for(shape: nat.Shape, device) -> torch.Tensor:
     if size == 0:
         nat.check(nat.lib().rsa_plan(C.byref(shape), None, None))
     return torch.empty(size, dtype=torch.uint8, device=device)
+
+
+def _checked_workspace(workspace, shape: nat.Shape, device) -> torch.Tensor:
+    """The caller's workspace, checked against this shape (a workspace sized for
+    a smaller problem would be overrun on the device), or a fresh one."""
+    if workspace is None:
+        return workspace_for(shape, device)
+    need = nat.lib().rsa_workspace_size(C.byref(shape))
+    if workspace.device != device or workspace.numel() * workspace.element_size() < need:
+        raise ShapeError(f"workspace holds {workspace.numel() * workspace.element_size()} bytes on "
+                         f"{workspace.device}; this shape needs {need} bytes on {device}")
+    if not workspace.is_contiguous():
+        raise ShapeError("workspace must be contiguous")
+    return workspace
+
+
+def _check_lse(lse, rows: int, device) -> None:
+    if lse is None:
+        return
+    if lse.dtype != torch.float32 or lse.numel() < rows or not lse.is_contiguous():
+        raise ShapeError(f"lse must be a contiguous float32 tensor of >= {rows} entries, "
+                         f"got {lse.dtype} with {lse.numel()}")
+    if device.type == "cuda" and lse.device != device:
+        raise ShapeError(f"lse is on {lse.device}, inputs on {device}")
 
 
 def _view(ws: torch.Tensor, offset: int, dtype, shape) -> torch.Tensor:
@@ -172,15 +207,16 @@ def block_sparse_attention(q_v, k, v, mask, grid: BlockGrid, counters: dict | No
         raise ShapeError(f"q_v has {q_v.shape[0]} rows, expected {grid.t_video} (the grid's video tokens)")
     if tuple(k.shape) != tuple(v.shape):
         raise ShapeError(f"k shape {tuple(k.shape)} != v shape {tuple(v.shape)}")
+    if k.shape[0] != grid.t_video + grid.t_text or k.shape[1] != q_v.shape[1]:
+        raise ShapeError(f"k has shape {tuple(k.shape)}, expected ({grid.t_video + grid.t_text}, "
+                         f"{q_v.shape[1]}) (video + text tokens of the grid, head_dim of q_v)")
     empty = ~bm.any(dim=1)
     if bool(empty.any()):
         raise EmptyRowError(f"mask rows {torch.nonzero(empty).flatten().tolist()} retain no key block")
     t_v, d = q_v.shape[0], q_v.shape[1]
     t_t = k.shape[0] - t_v
-    qv = _as_tensor(q_v, dev)
+    qv, kk, vv = _promote(dev, q_v, k, v)
     q = torch.cat([qv, torch.zeros(t_t, d, dtype=qv.dtype, device=dev)]).contiguous()
-    kk = _as_tensor(k, dev).contiguous()
-    vv = _as_tensor(v, dev).contiguous()
     shape = nat.make_shape(1, t_v, t_t, d, grid.block, str(q.dtype).replace("torch.", ""), kernel,
                            ragged_video=grid.ragged)
     ws = workspace_for(shape, dev)
@@ -197,7 +233,7 @@ def block_sparse_attention(q_v, k, v, mask, grid: BlockGrid, counters: dict | No
         counters["inner_product_ops"] = counters.get("inner_product_ops", 0) + ops
     o_video, ld = out[:t_v], lse[:t_v].to(torch.float64)
     if host:
-        return o_video.cpu().numpy().astype(q_v.dtype), ld.cpu().numpy()
+        return o_video.cpu().numpy(), ld.cpu().numpy()
     return o_video, ld
 
 
@@ -215,9 +251,7 @@ def text_full_attention(q_t, k, v, block: int = 128):
         return (np.empty((0, v.shape[1]), dtype=q_t.dtype) if host
                 else torch.empty(0, v.shape[1], dtype=q_t.dtype, device=q_t.device))
     dev = _device()
-    q = _as_tensor(q_t, dev).contiguous()
-    kk = _as_tensor(k, dev).contiguous()
-    vv = _as_tensor(v, dev).contiguous()
+    q, kk, vv = _promote(dev, q_t, k, v)
     out = torch.empty_like(q)
     code = nat.DTYPE_CODES[str(q.dtype).replace("torch.", "")]
     nat.check(nat.lib().rsa_text_full_attention(1, q.shape[0], kk.shape[0], q.shape[1], int(block),
@@ -240,16 +274,26 @@ def rectified_sparse_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor
                                variant: str = "sparse-rectified", sparsity: float | None = None,
                                kernel: str = "auto", lse: torch.Tensor | None = None,
                                workspace: torch.Tensor | None = None,
-                               check_status: bool = False, heads_per_chunk: int = 1,
+                               check_status: bool = True, status: torch.Tensor | None = None,
+                               heads_per_chunk: int = 1,
                                grid_dims: tuple | None = None, morton: bool = False,
                                ragged_video: bool = False) -> torch.Tensor:
     """Rectified block-sparse attention for every (batch, head) of q/k/v
     ([..., T, d], the last ``num_text_tokens`` rows text).  ``sparsity=s`` is
     shorthand for top_k_fraction = 1 - s with p = 0, r = 0, no forced text.
-    CUDA tensors: stream-ordered, no host synchronisation unless
-    ``check_status``.  Host tensors (the end-to-end call): the copies in and
-    out are pipelined with the compute over chunks of ``heads_per_chunk``
-    heads (rsa_forward_host) and the host output is returned.
+    Errors are the reference's exceptions (errors.py).  Shape / config errors
+    raise before any launch; the device-side ones (non-finite input ->
+    ShapeError, degenerate reallocation row -> DegenerateRowError, empty mask
+    row -> EmptyRowError; core.py:23-31, ipar.py:62-64, kernel.py:85-87) are
+    raised eagerly like the reference does when ``check_status`` (default),
+    which synchronises the stream once per call.  A model loop that must not
+    synchronise passes ``check_status=False`` and a zeroed int32[4] CUDA tensor
+    ``status``: every call ORs its flags into it on the stream (no sync), and
+    ``raise_for_status(status)`` raises the first error at the caller's next
+    synchronisation point.  Host tensors (the end-to-end call): the copies in
+    and out are pipelined with the compute over chunks of ``heads_per_chunk``
+    heads (rsa_forward_host), the flags of every chunk are kept, checked after
+    the final synchronisation, and the host output is returned.
     ``morton=True`` (needs ``grid_dims`` = (t, h, w) of the video tokens):
     the pipeline runs on the Morton-reordered problem, as the reference
     harness's ``morton_reorder`` option does (harness.py:172-173), with the
@@ -277,8 +321,10 @@ def rectified_sparse_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor
             raise ShapeError("morton=True needs CUDA tensors (use reorder_morton for host arrays)")
         if k.is_cuda or v.is_cuda:
             raise ShapeError("q, k and v must all be host tensors or all CUDA tensors")
-        return _forward_from_host(q, k, v, shape, cfg, lse, workspace, heads_per_chunk)
+        return _forward_from_host(q, k, v, shape, cfg, lse, workspace, heads_per_chunk, status)
     q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+    workspace = _checked_workspace(workspace, shape, q.device)
+    _check_lse(lse, heads * T, q.device)
     if morton:
         from .errors import MissingGridError
         from .reorder import device_permutation, permuted_forward
@@ -288,23 +334,39 @@ def rectified_sparse_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor
         if t * hh * w != T - t_t:
             raise ShapeError(f"grid_dims product {t * hh * w} != T_v={T - t_t}")
         out = permuted_forward(q, k, v, shape, cfg, device_permutation(grid_dims, q.device), lse, workspace)
-        if check_status:
-            nat.check(nat.lib().rsa_check_device_status(_ptr(workspace), _stream()))
-        return out
-    if workspace is None:
-        workspace = workspace_for(shape, q.device)
-    out = torch.empty_like(q)
-    nat.check(nat.lib().rsa_forward(C.byref(shape), C.byref(cfg), _ptr(q), _ptr(k), _ptr(v),
-                                    _ptr(out), _ptr(lse), _ptr(workspace), _stream()))
-    if check_status:
-        nat.check(nat.lib().rsa_check_device_status(_ptr(workspace), _stream()))
+    else:
+        out = torch.empty_like(q)
+        nat.check(nat.lib().rsa_forward(C.byref(shape), C.byref(cfg), _ptr(q), _ptr(k), _ptr(v),
+                                        _ptr(out), _ptr(lse), _ptr(workspace), _stream()))
+    _report_status(workspace, status, check_status)
     return out
+
+
+def _report_status(workspace: torch.Tensor, status: torch.Tensor | None, check: bool) -> None:
+    if status is not None:
+        if status.dtype != torch.int32 or status.numel() < 4 or status.device != workspace.device:
+            raise ShapeError("status must be an int32 CUDA tensor of 4 entries on the inputs' device")
+        nat.check(nat.lib().rsa_accumulate_status(_ptr(workspace), _ptr(status), _stream()))
+    if check:
+        nat.check(nat.lib().rsa_check_device_status(_ptr(workspace), _stream()))
+
+
+def new_status(device=None) -> torch.Tensor:
+    """A zeroed status accumulator for ``rectified_sparse_attention(status=...)``."""
+    return torch.zeros(4, dtype=torch.int32, device=device if device is not None else _device())
+
+
+def raise_for_status(status: torch.Tensor) -> None:
+    """Raise the reference exception for the flags accumulated in ``status``
+    (synchronises with the stream that last wrote it)."""
+    flags = status.detach().to("cpu", torch.int32).contiguous()
+    nat.check(nat.lib().rsa_status_from_flags(_ptr(flags)))
 
 
 _STAGING: dict = {}
 
 
-def _forward_from_host(q, k, v, shape, cfg, lse, workspace, heads_per_chunk):
+def _forward_from_host(q, k, v, shape, cfg, lse, workspace, heads_per_chunk, status=None):
     """Host tensors in, host tensor out: rsa_forward_host pipelines the
     host->device copies, the three kernels and the device->host copy over
     chunks of heads.  Inputs should be page-locked (``pin_memory()``) for the
@@ -319,12 +381,17 @@ def _forward_from_host(q, k, v, shape, cfg, lse, workspace, heads_per_chunk):
         _STAGING.clear()
         bufs = [torch.empty(q.shape, dtype=q.dtype, device=dev) for _ in range(4)]
         _STAGING[key] = bufs
-    dq, dk, dv, dout = bufs
+    dq, dk, dv, dout = bufs[:4]
     if workspace is None:
-        workspace = workspace_for(shape, dev)
+        if len(bufs) == 4:
+            bufs.append(workspace_for(shape, dev))
+        workspace = bufs[4]
+    workspace = _checked_workspace(workspace, shape, dev)
+    _check_lse(lse, int(np.prod(q.shape[:-1])), dev)
     out = torch.empty(q.shape, dtype=q.dtype, pin_memory=q.is_pinned())
     nat.check(nat.lib().rsa_forward_host(C.byref(shape), C.byref(cfg), _ptr(q), _ptr(k), _ptr(v), _ptr(out),
                                          _ptr(dq), _ptr(dk), _ptr(dv), _ptr(dout), _ptr(lse),
                                          _ptr(workspace), int(heads_per_chunk), _stream()))
-    torch.cuda.current_stream().synchronize()
+    # flags of every head chunk (rsa_forward_host clears them once); synchronises
+    _report_status(workspace, status, True)
     return out

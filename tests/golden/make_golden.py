@@ -194,6 +194,69 @@ def large_goldens(rt) -> None:
     np.savez_compressed(HERE / "large_masks.npz", **out)
 
 
+# Query blocks whose outputs are recorded at the headline shapes (the full
+# reference head is run; only these rows are stored, to keep the fixture small).
+def headline_query_blocks(n_q: int, count: int = 64) -> np.ndarray:
+    rng = np.random.default_rng(2511)
+    pick = set(rng.choice(n_q, count - 2, replace=False).tolist()) | {0, n_q - 1}
+    return np.array(sorted(pick), dtype=np.int64)
+
+
+HEADLINE_ROWS = np.arange(0, 128, 16)      # 8 rows of every sampled query block
+
+
+def headline_goldens(rt) -> None:
+    """The whole reference pipeline (sparse-rectified, f=0.1, p=0) on one
+    HunyuanVideo head and one Wan head, outputs recorded on sampled rows; and
+    HunyuanVideo masks at the cumulative-weight rule p = 0.3 (paper) / 0.5."""
+    import time
+    out = {}
+    spec = rt.SyntheticSpec(seed=42, t_v=HV["t_v"], t_t=HV["t_t"], d=HV["d"],
+                            block=HV["block"], grid_dims=HV["grid"],
+                            locality_strength=1.0, text_norm_boost=2.0,
+                            intra_block_noise=0.3, precision="single")
+    prob = rt.gen_synthetic(spec)
+    hv = [round_to_bf16(getattr(prob, n)) for n in ("q_video", "q_text", "k", "v")]
+    rng = np.random.default_rng(42)
+    t = WAN["t_v"]
+    wan = [round_to_bf16(rng.standard_normal((t, WAN["d"])).astype(np.float32)) for _ in range(3)]
+    wan = [wan[0], np.zeros((0, WAN["d"]), dtype=np.float32), wan[1], wan[2]]
+    for tag, (qv, qt, k, v), block in (("hv", hv, HV["block"]), ("wan", wan, WAN["block"])):
+        t0 = time.perf_counter()
+        res = run_ref(rt, qv, qt, k, v, block, 0.1, 0.0, 0, False, "sparse-rectified")
+        dt = time.perf_counter() - t0
+        qb = headline_query_blocks(qv.shape[0] // block)
+        rows = (qb[:, None] * block + HEADLINE_ROWS[None, :]).ravel()
+        lse_rows = (qb[:, None] * block + np.arange(block)[None, :]).ravel()
+        out[f"{tag}_query_blocks"] = qb
+        out[f"{tag}_rows"] = rows
+        out[f"{tag}_o_video_rows"] = res.output.o_video[rows]
+        out[f"{tag}_o_text"] = res.output.o_text
+        out[f"{tag}_lse_blocks"] = res.output.row_log_denominators[lse_rows]
+        out[f"{tag}_mask"] = np.packbits(res.sparse_mask.mask, axis=1)
+        out[f"{tag}_seconds"] = np.array([dt])
+        print(f"{tag}: reference pipeline {dt:.1f} s")
+    for p in (0.3, 0.5):
+        prob_hv = rt.AttentionProblem(q_video=hv[0], q_text=hv[1], k=hv[2], v=hv[3],
+                                      d=HV["d"], block=HV["block"])
+        from rectattn.core import partition, pool_problem
+        from rectattn.ipar import implicit_full_attention
+        from rectattn.masks import build_sparse_mask
+        from rectattn.rectify import rectification_factors
+        grid = partition(prob_hv)
+        imp = implicit_full_attention(prob_hv, pool_problem(prob_hv, grid), grid)
+        cfg = rt.SparsityConfig(top_k_fraction=0.1, weight_threshold=p,
+                                adjacency_radius=0, force_text_blocks=False)
+        sparse = build_sparse_mask(imp.a_pool, cfg, grid)
+        out[f"hv_p{p}_mask"] = np.packbits(sparse.mask, axis=1)
+        out[f"hv_p{p}_r"] = rectification_factors(imp.a_pool, sparse).r
+        k_floor = int(np.ceil(0.1 * grid.n_kv))
+        binds = int((sparse.mask.sum(axis=1) > k_floor).sum())
+        out[f"hv_p{p}_rows_binding"] = np.array([binds])
+        print(f"HV p={p}: cumulative-weight rule binds on {binds} of {grid.n_q} rows")
+    np.savez_compressed(HERE / "headline_outputs.npz", **out)
+
+
 MORTON_GRIDS = ((2, 4, 4), (3, 5, 7), (1, 60, 64), (29, 4, 6), (5, 16, 12))
 
 
@@ -287,6 +350,11 @@ def main():
         import rectattn as rt
         diag_goldens(rt)
         return
+    if "--headline-only" in sys.argv:
+        sys.path.insert(0, "/root/reference/pkg/src")
+        import rectattn as rt
+        headline_goldens(rt)
+        return
     if "--morton-only" in sys.argv:
         sys.path.insert(0, "/root/reference/pkg/src")
         import rectattn as rt
@@ -303,6 +371,7 @@ def main():
         harness_goldens(rt)
         if "--no-large" not in sys.argv:
             large_goldens(rt)
+            headline_goldens(rt)
     (HERE / "README.md").write_text(
         "Golden fixtures generated by `python tests/golden/make_golden.py` from the\n"
         "reference package at /root/reference/pkg (see the script docstring).\n"

@@ -211,3 +211,29 @@ def test_oracle_against_live_reference_when_present():
             got = O.pipeline(qv, qt, k, v, 8, 0.3, 0.4, 1, True, variant)
             np.testing.assert_array_equal(got["o_video"], ref.output.o_video)
             np.testing.assert_array_equal(got["mask"], ref.sparse_mask.mask)
+
+
+@pytest.mark.parametrize("tag", ["hv", "wan"])
+def test_oracle_matches_reference_at_headline_shapes(tag):
+    """The oracle restatement reproduces the reference's own outputs on one
+    full HunyuanVideo / Wan 2.1 head bit for bit (mask, sampled video rows of
+    64 query blocks, all text rows, row log-denominators) -- the pin for the
+    GPU headline parity tests (test_headline_parity.py)."""
+    from threadpoolctl import threadpool_limits
+    from conftest import load_golden
+    g = load_golden("headline_outputs.npz")
+    if tag == "hv":
+        inputs = O.gen_synthetic(42, 118784, 256, 128, 128, (29, 64, 64), 1.0, 2.0, 0.3)
+    else:
+        rng = np.random.default_rng(42)
+        qv, k, v = (rng.standard_normal((75520, 128)).astype(np.float32) for _ in range(3))
+        inputs = (qv, np.zeros((0, 128), dtype=np.float32), k, v)
+    qv, qt, k, v = (O.round_to_bf16(x) for x in inputs)
+    qb = g[f"{tag}_query_blocks"]
+    with threadpool_limits(1):
+        ref = O.pipeline(qv, qt, k, v, 128, 0.1, 0.0, 0, False, "sparse-rectified", query_blocks=qb)
+    np.testing.assert_array_equal(np.packbits(ref["mask"], axis=1), g[f"{tag}_mask"])
+    np.testing.assert_array_equal(ref["o_video"][g[f"{tag}_rows"]], g[f"{tag}_o_video_rows"])
+    np.testing.assert_array_equal(ref["o_text"], g[f"{tag}_o_text"])
+    lse_rows = (qb[:, None] * 128 + np.arange(128)[None, :]).ravel()
+    np.testing.assert_array_equal(ref["lse"][lse_rows], g[f"{tag}_lse_blocks"])
