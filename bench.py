@@ -17,10 +17,15 @@ Multi-GPU (torchrun, one rank per GPU): the call's heads are sharded across
 ranks (strong scaling of one fixed call, no collective on the data path);
 ms/call is the max over ranks of the device time.
 
-``--impl reference`` times the reference algorithm's CPU implementation (the
-oracle port in oracle/, the reference itself being a numpy package that
-cannot travel to the GPU box) on the host cores, on a bounded sample of the
-same call, extrapolated to ms/call.
+``--impl reference`` times the reference's own CPU implementation -- the
+unmodified rectattn package installed into baseline/_ref (pip --target; it
+travels to the GPU box with the repo), through its public
+rectified_attention_pipeline -- on the host cores: one COMPLETE head per step
+(every query block), the call = heads x the median head (heads are identical
+independent problems), in the pinned BLAS environment, plus one
+head in the as-shipped environment.  The GPU arm's `cpu_baseline` is the same
+measurement on one head.  Without baseline/_ref the oracle port is timed
+instead (kind "port").
 """
 
 from __future__ import annotations
@@ -71,7 +76,16 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-chunk", type=int, default=1, help="heads per pipelined chunk of the e2e call")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-blocks", type=int, default=96)
+    ap.add_argument("--cpu-heads", type=int, default=1, help="complete heads timed by the cpu_baseline leg")
+    ap.add_argument("--cpu-warmup", type=int, default=0)
+    ap.add_argument("--cpu-worker", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--no-as-shipped", action="store_true",
+                    help="reference arm: skip the one-head timing in the as-shipped BLAS environment")
+    ap.add_argument("--as-shipped-timeout", type=float, default=150.0)
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the sparsity sweep / Wan / dense legs appended to the N=1 line")
+    ap.add_argument("--heads-per-group", type=int, default=1,
+                    help="--input-layout seq: heads per overlapped all-to-all group")
     ap.add_argument("--profile", action="store_true", help="fewer steps, no side legs (for ncu)")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                     help="gloo: plumbing check of the multi-rank path (ranks may share one GPU)")
@@ -192,77 +206,143 @@ def synth_inputs(torch, cfg, heads, seed, device):
 
 
 # ----------------------------------------------------------------------------- CPU legs
+#
+# The reference is a numpy package (rectattn); it is installed, unmodified,
+# into baseline/_ref by `pip install --target baseline/_ref` and
+# travels to the GPU box with the repo.  Its public entry point
+# rectattn.rectified_attention_pipeline is timed on COMPLETE heads (every query
+# block, the text queries, the pooled path and the rectification) in a worker
+# subprocess, so the BLAS threading environment is set before numpy loads:
+#   pinned     OPENBLAS_NUM_THREADS=1, RECTATTN_THREADS=<all cores> (one BLAS
+#              thread inside each of the reference's per-query-block threads)
+#   as shipped the environment as found (OpenBLAS's own thread pool inside each
+#              reference thread -- kernel.py:32-40 default)
+# A call is heads x one head's time: heads are identical independent problems
+# (SPEC.md:112); only the head count is extrapolated, never query blocks.
+# Without baseline/_ref the oracle port (oracle/rsa_oracle.py, bit-identical on
+# the goldens) is timed the same way and the line says kind "port".
 
-def cpu_reference_sample(cfg, f, variant, sample_blocks, seed=42):
-    """Time the oracle port (the reference algorithm, numpy) on one head's
-    pooled path plus `sample_blocks` query blocks of the sparse kernel and the
-    head's text queries; extrapolate to the whole call."""
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+REF_DIR = ROOT / "baseline" / "_ref"
+
+
+def _bf16_round(np, x):
+    """Round-to-nearest-even fp32 -> bf16 values (the GPU arm's inputs)."""
+    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
+    return r.astype(np.uint32).view(np.float32)
+
+
+def cpu_worker(args):
+    """(subprocess) time `--cpu-heads` complete heads after `--cpu-warmup`."""
     import numpy as np
-    from threadpoolctl import threadpool_limits
-    from oracle import rsa_oracle as O
-    # single-threaded BLAS inside the oracle's per-query-block thread pool (all
-    # host cores): numpy may already have started multi-threaded OpenBLAS when
-    # torch was imported, which oversubscribes the cores 16x
-    # two heads (seeds 42, 43; BASELINE.md section 3: extrapolate from >= 2 heads)
-    with threadpool_limits(limits=1, user_api="blas"):
-        runs = [_cpu_reference_sample(np, O, cfg, f, variant, sample_blocks, seed + i) for i in range(2)]
-    per_head = sum(r["per_head_s"] for r in runs) / len(runs)
-    return {"ms_per_call": per_head * cfg["heads"] * 1e3, "sample_s": sum(r["sample_s"] for r in runs),
-            "per_head_s": per_head, "cores": runs[0]["cores"],
-            "sample": runs[0]["sample"].replace(f"1 head (seed {seed}) of", f"2 heads (seeds {seed}, {seed + 1}; "
-                                                                           f"mean per head) of")}
-
-
-def _cpu_reference_sample(np, O, cfg, f, variant, sample_blocks, seed):
+    cfg = CONFIGS[args.config]
+    f = 1.0 - args.sparsity
     t_v, t_t, d, B = cfg["t_v"], cfg["t_t"], cfg["d"], cfg["block"]
-    ragged = cfg.get("ragged", False)
-    if t_t and ragged:
-        # gen_synthetic needs full blocks: full-block problem + N(0,1) rows for the ragged block
-        tf = (t_v // B) * B
-        qv, qt, k, v = O.gen_synthetic(seed, tf, t_t, d, B, (1, tf // B, B), 1.0, 2.0, 0.3)
-        rng = np.random.default_rng(seed)
-        ex = [rng.standard_normal((t_v - tf, d)).astype(np.float32) for _ in range(3)]
-        qv = np.concatenate([qv, ex[0]])
-        k = np.concatenate([k[:tf], ex[1], k[tf:]])
-        v = np.concatenate([v[:tf], ex[2], v[tf:]])
-    elif t_t:
-        qv, qt, k, v = O.gen_synthetic(seed, t_v, t_t, d, B, cfg["grid"], 1.0, 2.0, 0.3)
+    kind = "reference" if (REF_DIR / "rectattn").is_dir() and not cfg.get("ragged") else "port"
+    if kind == "reference":
+        sys.path.insert(0, str(REF_DIR))
+        import rectattn as rt
     else:
-        rng = np.random.default_rng(seed)
-        qv, k, v = (rng.standard_normal((t_v, d)).astype(np.float32) for _ in range(3))
-        qt = np.zeros((0, d), np.float32)
-    qv, qt, k, v = (O.round_to_bf16(x) for x in (qv, qt, k, v))
-    t0 = time.perf_counter()
-    pooled = O.pool(qv, k, v, t_t, B, ragged)
-    imp = O.implicit_attention(pooled, d, B, t_t)
-    scores = O.pooled_scores(pooled, d)
-    g = O.gain(scores, B, pooled["lens"], pooled["q_lens"])
-    e = O.pooling_error(qv, k, pooled, B, d)
-    sel = O.select_mask(imp["a_pool"], f, 0.0, 0, False, pooled["n_q"])
-    _ = g > e
-    r = O.rect_factors(imp["a_pool"], sel["mask"])
-    t_pooled = time.perf_counter() - t0
-    n = pooled["n_q"]
-    rows = np.linspace(0, n - 1, min(sample_blocks, n)).astype(int)
-    t0 = time.perf_counter()
-    O.sparse_attention(qv, k, v, sel["mask"], pooled["lens"], B, query_blocks=rows)
-    t_kernel = (time.perf_counter() - t0) * n / len(rows)
-    t0 = time.perf_counter()
-    O.text_attention(qt, k, v, B)
-    t_text = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    applied = ~sel["mask"] & (g > e)
-    O.rectify(np.zeros((t_v, d), np.float32), r, imp["a_pool"], applied, pooled["v_pool"], B)
-    t_rect = time.perf_counter() - t0
-    per_head = t_pooled + t_kernel + t_text + t_rect
-    sample_s = t_pooled + t_kernel * len(rows) / n + t_text + t_rect
-    return {"ms_per_call": per_head * cfg["heads"] * 1e3, "sample_s": sample_s,
-            "per_head_s": per_head, "sample": (f"1 head (seed {seed}) of {cfg['heads']}: full pooled path + "
-                                               f"{len(rows)}/{n} query blocks of the sparse kernel + all text "
-                                               f"queries + rectification, extrapolated x{n}/{len(rows)} kernel, "
-                                               f"x{cfg['heads']} heads"),
-            "cores": os.cpu_count() or 1}
+        from oracle import rsa_oracle as O
+    distinct = max(1, min(4, cfg["heads"]))
+    cache = {}
+
+    def head(seed):
+        if seed in cache:
+            return cache[seed]
+        if t_t:
+            if kind == "reference":
+                p = rt.gen_synthetic(rt.SyntheticSpec(seed=seed, t_v=t_v, t_t=t_t, d=d, block=B,
+                                                      grid_dims=cfg["grid"], locality_strength=1.0,
+                                                      text_norm_boost=2.0, intra_block_noise=0.3,
+                                                      precision="single"))
+                arrs = (p.q_video, p.q_text, p.k, p.v)
+            else:
+                tf = (t_v // B) * B
+                arrs = O.gen_synthetic(seed, tf, t_t, d, B, (1, tf // B, B) if tf != t_v else cfg["grid"],
+                                       1.0, 2.0, 0.3)
+                if tf != t_v:   # ragged final video block: N(0,1) rows appended
+                    rng = np.random.default_rng(seed)
+                    ex = [rng.standard_normal((t_v - tf, d)).astype(np.float32) for _ in range(3)]
+                    qv, qt, k, v = arrs
+                    arrs = (np.concatenate([qv, ex[0]]), qt, np.concatenate([k[:tf], ex[1], k[tf:]]),
+                            np.concatenate([v[:tf], ex[2], v[tf:]]))
+        else:   # Wan: T_t = 0, which gen_synthetic rejects -> N(0,1) rows (SURVEY 8d)
+            rng = np.random.default_rng(seed)
+            qv, k, v = (rng.standard_normal((t_v, d)).astype(np.float32) for _ in range(3))
+            arrs = (qv, np.zeros((0, d), np.float32), k, v)
+        cache[seed] = tuple(_bf16_round(np, x) for x in arrs)
+        return cache[seed]
+
+    times = []
+    for i in range(args.cpu_warmup + args.cpu_heads):
+        qv, qt, k, v = head(42 + i % distinct)
+        t0 = time.perf_counter()
+        if kind == "reference":
+            prob = rt.AttentionProblem(q_video=qv, q_text=qt, k=k, v=v, d=d, block=B)
+            conf = rt.SparsityConfig(top_k_fraction=f, weight_threshold=args.weight_threshold,
+                                     adjacency_radius=0, force_text_blocks=False)
+            rt.rectified_attention_pipeline(prob, conf, variant=args.variant)
+        else:
+            O.pipeline(qv, qt, k, v, B, f, args.weight_threshold, 0, False, args.variant,
+                       ragged=cfg.get("ragged", False))
+        dt = time.perf_counter() - t0
+        if i >= args.cpu_warmup:
+            times.append(dt)
+    print(json.dumps({"kind": kind, "head_s": times, "cores": os.cpu_count() or 1,
+                      "distinct_heads": distinct}), flush=True)
+
+
+def cpu_heads(args, heads: int, warmup: int, pinned: bool = True, timeout: float | None = None):
+    """Run cpu_worker in a subprocess with the pinned or as-shipped BLAS env."""
+    env = dict(os.environ)
+    cores = os.cpu_count() or 1
+    if pinned:
+        env.update(OPENBLAS_NUM_THREADS="1", OMP_NUM_THREADS="1", MKL_NUM_THREADS="1",
+                   RECTATTN_THREADS=str(cores))
+    else:
+        for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS", "RECTATTN_THREADS"):
+            env.pop(k, None)
+    cmd = [sys.executable, str(Path(__file__).resolve()), "--cpu-worker", "--config", args.config,
+           "--sparsity", str(args.sparsity), "--weight-threshold", str(args.weight_threshold),
+           "--variant", args.variant, "--cpu-heads", str(heads), "--cpu-warmup", str(warmup)]
+    try:
+        res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=timeout, cwd=str(ROOT))
+    except subprocess.TimeoutExpired:
+        return {"timed_out_s": timeout}
+    if res.returncode != 0:
+        raise RuntimeError(f"cpu worker failed: {res.stderr[-2000:]}")
+    out = json.loads(res.stdout.strip().splitlines()[-1])
+    out["env"] = ("OPENBLAS_NUM_THREADS=1, RECTATTN_THREADS=%d" % cores) if pinned else "as shipped (default env)"
+    return out
+
+
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def config_dict(cfg, f, args, world, ulysses=False) -> dict:
+    """The configuration both arms report (identical keys and values)."""
+    return {"workload": cfg["label"], "heads": cfg["heads"], "t_video": cfg["t_v"], "t_text": cfg["t_t"],
+            "head_dim": cfg["d"], "block": cfg["block"], "top_k_fraction": round(f, 6),
+            "weight_threshold": args.weight_threshold, "adjacency_radius": 0, "force_text_blocks": False,
+            "variant": args.variant,
+            "parallelism": (f"Ulysses seq->head all-to-all x{world} ({args.dist_backend})" if ulysses
+                            else f"head-sharded x{world}"),
+            "l2": "inputs 2.2 GB >> 126 MB L2 (no flush needed)" if args.config != "cfg1"
+            else "inputs 6 MB; L2 resident"}
+
+
+def cpu_sample_text(res, heads) -> str:
+    n = len(res["head_s"])
+    return (f"{n} complete heads (every query block, text queries, pooled path, rectification; "
+            f"{res['distinct_heads']} distinct seeds) of {heads}, median per head x {heads} heads")
 
 
 # ----------------------------------------------------------------------------- main legs
@@ -273,24 +353,109 @@ def run_reference(args):
         return
     cfg = CONFIGS[args.config]
     f = 1.0 - args.sparsity
-    samples = []
-    for i in range(args.warmup + args.steps):
-        res = cpu_reference_sample(cfg, f, args.variant, max(8, args.cpu_sample_blocks // 4))
-        if i >= args.warmup:
-            samples.append(res)
-    ms = statistics.median(s["ms_per_call"] for s in samples)
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    res = cpu_heads(args, args.steps, args.warmup)
+    per_head = statistics.median(res["head_s"])
+    ms = per_head * cfg["heads"] * 1e3
+    cpu = {"value": ms, "unit": "ms/call", "cores": res["cores"], "kind": res["kind"],
+           "sample": cpu_sample_text(res, cfg["heads"]), "env": res["env"], "cpu_model": cpu_model(),
+           "per_head_s": per_head, "head_s": res["head_s"]}
+    if not args.no_as_shipped:
+        shipped = cpu_heads(args, 1, 0, pinned=False, timeout=args.as_shipped_timeout)
+        cpu["as_shipped"] = ({"timed_out_after_s": shipped["timed_out_s"]} if "timed_out_s" in shipped else
+                             {"per_head_s": shipped["head_s"][0], "ms_per_call": shipped["head_s"][0] *
+                              cfg["heads"] * 1e3, "env": shipped["env"], "sample": "1 complete head"})
     line = {
-        "impl": "reference", "metric": METRIC, "value": ms, "unit": "ms/call", "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": ms, "unit": "ms/call", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": cfg["label"], "heads": cfg["heads"], "t_video": cfg["t_v"],
-                   "t_text": cfg["t_t"], "head_dim": cfg["d"], "block": cfg["block"],
-                   "top_k_fraction": round(f, 6), "variant": args.variant},
-        "cpu_baseline": {"value": ms, "unit": "ms/call", "cores": samples[0]["cores"], "kind": "port",
-                         "sample": samples[0]["sample"]},
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference gen_synthetic, "
+        "bf16-rounded)", "config": config_dict(cfg, f, args, world, args.input_layout == "seq" and world > 1),
+        "cpu_baseline": cpu,
         "e2e": {"value": ms, "unit": "ms/call", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def _measure(torch, nat, lib, shape, conf, q, k, v, out, ws, steps, warm):
+    """Median per-stage event times of `steps` calls (K1, K2, K3) and the whole call."""
+    import ctypes as C_
+    from paper_2511_19835_b200.pipeline import _ptr, _stream
+    st, sp = torch.cuda.current_stream(), _stream()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    rows = []
+    for i in range(warm + steps):
+        ev[0].record(st)
+        nat.check(lib.rsa_pool(C_.byref(shape), _ptr(q), _ptr(k), _ptr(v), _ptr(ws), sp))
+        ev[1].record(st)
+        nat.check(lib.rsa_select(C_.byref(shape), C_.byref(conf), _ptr(ws), sp))
+        ev[2].record(st)
+        nat.check(lib.rsa_attention(C_.byref(shape), C_.byref(conf), _ptr(q), _ptr(k), _ptr(v), _ptr(out),
+                                    None, _ptr(ws), sp))
+        ev[3].record(st)
+        torch.cuda.synchronize()
+        if i >= warm:
+            rows.append([ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3]),
+                         ev[0].elapsed_time(ev[3])])
+    nat.check(lib.rsa_check_device_status(_ptr(ws), sp))
+    med = [statistics.median(r[j] for r in rows) for j in range(4)]
+    return {"pool": med[0], "select": med[1], "attention": med[2], "call": med[3]}
+
+
+def _exec_flops(torch, nat, ws, shape, grid, heads, d, T, t_t, block, dev):
+    """Executed FLOPs (metrics.py:85 convention + text rows) and realized sparsity."""
+    L = nat.layout(shape)
+    bits = ws[L["mask_bits"]:L["mask_bits"] + heads * grid.n_q * grid.n_kv].view(heads, grid.n_q, grid.n_kv)
+    mask = (bits & 1).to(torch.int64)
+    lens = torch.full((grid.n_kv,), block, dtype=torch.int64, device=dev)
+    if grid.n_text_blocks:
+        lens[-1] = grid.last_text_block_len
+    lens[grid.n_q - 1] = grid.last_video_block_len
+    qlens = torch.full((grid.n_q,), block, dtype=torch.int64, device=dev)
+    qlens[-1] = grid.last_video_block_len
+    pairs = int((mask * lens[None, None, :] * qlens[None, :, None]).sum().item())
+    flops = 4 * d * pairs + 4 * t_t * T * d * heads
+    return flops, 1.0 - float(mask.sum().item()) / (heads * grid.n_q * grid.n_kv)
+
+
+def extras(torch, nat, lib, workspace_for, args, q, k, v, out, ws, dev, peak_burst):
+    """BASELINE.json configs[2]-[3] on the same run: the sparsity sweep at the
+    HunyuanVideo shape (IPAR+GAPR on = sparse-rectified, off = sparse-
+    unrectified, and our own dense kernel = the `full` variant) and the Wan 2.1
+    shape at 90 %; 5 timed calls after 2 warm-ups each."""
+    hv = CONFIGS["hv"]
+    heads, T, d = q.shape[0], q.shape[1], q.shape[2]
+    shape = nat.make_shape(heads, hv["t_v"], hv["t_t"], d, hv["block"], "bfloat16", args.kernel)
+    grid = nat.plan(shape)
+    res = {"sweep": [], "note": "ms/call (CUDA events, median of 5 after 2 warm-up); frac = K3 executed "
+                                "TFLOP/s / measured burst bf16 peak"}
+    for f in (0.5, 0.25, 0.1, 0.05):
+        for variant in ("sparse-rectified", "sparse-unrectified"):
+            conf = nat.make_config(f, 0.0, 0, False, variant)
+            t = _measure(torch, nat, lib, shape, conf, q, k, v, out, ws, 5, 2)
+            fl, sp = _exec_flops(torch, nat, ws, shape, grid, heads, d, T, hv["t_t"], hv["block"], dev)
+            res["sweep"].append({"top_k_fraction": f, "variant": variant, "ms": t["call"], "kernels_ms": t,
+                                 "realized_sparsity": sp, "k3_tflops": fl / (t["attention"] * 1e-3) / 1e12,
+                                 "k3_frac": fl / (t["attention"] * 1e-3) / 1e12 / peak_burst})
+    conf = nat.make_config(1.0, 0.0, 0, False, "full")
+    t = _measure(torch, nat, lib, shape, conf, q, k, v, out, ws, 3, 1)
+    fl = 4 * T * T * d * heads
+    res["dense_full"] = {"ms": t["call"], "kernels_ms": t, "k3_tflops": fl / (t["attention"] * 1e-3) / 1e12,
+                         "k3_frac": fl / (t["attention"] * 1e-3) / 1e12 / peak_burst}
+    wan = CONFIGS["wan"]
+    qw, kw_, vw = synth_inputs(torch, wan, wan["heads"], 4321, dev)
+    ow = torch.empty_like(qw)
+    shape_w = nat.make_shape(wan["heads"], wan["t_v"], wan["t_t"], wan["d"], wan["block"], "bfloat16", args.kernel)
+    grid_w = nat.plan(shape_w)
+    ws_w = workspace_for(shape_w, dev)
+    conf = nat.make_config(0.1, 0.0, 0, False, "sparse-rectified")
+    t = _measure(torch, nat, lib, shape_w, conf, qw, kw_, vw, ow, ws_w, 5, 2)
+    fl, sp = _exec_flops(torch, nat, ws_w, shape_w, grid_w, wan["heads"], wan["d"], wan["t_v"], 0, wan["block"], dev)
+    res["wan"] = {"workload": wan["label"], "heads": wan["heads"], "t_video": wan["t_v"], "top_k_fraction": 0.1,
+                  "ms": t["call"], "kernels_ms": t, "realized_sparsity": sp,
+                  "k3_tflops": fl / (t["attention"] * 1e-3) / 1e12,
+                  "k3_frac": fl / (t["attention"] * 1e-3) / 1e12 / peak_burst}
+    del qw, kw_, vw, ow, ws_w
+    return res
 
 
 def run_ours(args):
@@ -357,25 +522,24 @@ def run_ours(args):
         tq, tk, tv = (x[None, :, t_v:].contiguous() for x in (qa, ka, va))
         del qa, ka, va
 
-        def uattn(q_, k_, v_, t_t_):
-            return rsa.rectified_sparse_attention(q_, k_, v_, num_text_tokens=t_t_, block=cfg["block"],
-                                                  top_k_fraction=f, weight_threshold=args.weight_threshold,
-                                                  variant=args.variant, kernel=args.kernel,
-                                                  workspace=ws)
+        groups = -(-(cfg["heads"] // world) // max(1, args.heads_per_group))
+        ukw = dict(block=cfg["block"], top_k_fraction=f, weight_threshold=args.weight_threshold,
+                   variant=args.variant, kernel=args.kernel, workspace=ws, check_status=False)
 
         def step(record=False):
             if record:
                 ev[0].record(st)
                 ev[1].record(st)
                 ev[2].record(st)
-            ulysses_attention(uq, uk, uv, tq, tk, tv, attn_fn=uattn)
+            ulysses_attention(uq, uk, uv, tq, tk, tv, heads_per_group=args.heads_per_group, **ukw)
             if record:
                 ev[3].record(st)
 
     for _ in range(args.warmup):
         c0 = nat.last_launch_count()
         step()
-        launches_per_step = nat.last_launch_count() - (0 if ulysses else c0)
+        # (a Ulysses step is `groups` rsa_forward calls; the counter holds the last one)
+        launches_per_step = nat.last_launch_count() * groups if ulysses else nat.last_launch_count() - c0
     nat.check(lib.rsa_check_device_status(_ptr(ws), sptr))
     torch.cuda.synchronize()
 
@@ -477,7 +641,7 @@ def run_ours(args):
     attn_ms = stage["attention"]
     per_rank_exec = flops_exec / world
     achieved = per_rank_exec / (attn_ms * 1e-3) / 1e12
-    peak = peaks["bf16_sustained"]
+    peak = peaks["bf16"]   # burst: K3 is timed on its own (per-stage events), not inside a seconds-long step
     traffic = None
     tp = ROOT / "profiles" / "attn_traffic.json"
     if tp.exists():
@@ -489,21 +653,15 @@ def run_ours(args):
         "metric": METRIC, "value": ms_step, "unit": "ms/call", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (gen_synthetic-style, torch RNG)",
-        "config": {"workload": cfg["label"], "heads": cfg["heads"], "t_video": cfg["t_v"], "t_text": cfg["t_t"],
-                   "head_dim": d, "block": cfg["block"], "top_k_fraction": round(f, 6),
-                   "weight_threshold": args.weight_threshold, "adjacency_radius": 0, "force_text_blocks": False,
-                   "variant": args.variant,
-                   "parallelism": (f"Ulysses seq->head all-to-all x{world} (NCCL)" if ulysses
-                                   else f"head-sharded x{world}"),
-                   "l2": "inputs 2.2 GB >> 126 MB L2 (no flush needed)" if args.config != "cfg1"
-                   else "inputs 6 MB; L2 resident", "kernel": args.kernel},
+        "config": config_dict(cfg, f, args, world, ulysses),
+        "kernel_choice": args.kernel,
         "tflops_effective": flops_exec / (ms_step * 1e-3) / 1e12,
         "tflops_dense_equivalent": flops_dense / (ms_step * 1e-3) / 1e12,
         "realized_sparsity": sparsity,
         "kernels_ms": stage,
         "roofline": {"bound": "tensor", "kernel": "attn_tc_kernel (K3+K4)", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                     "frac_of_burst": achieved / peaks["bf16"], "peak_src": peaks["src"] + " sustained",
+                     "frac_of_sustained": achieved / peaks["bf16_sustained"], "peak_src": peaks["src"] + " burst",
                      "traffic": traffic,
                      "algorithmic": f"{per_rank_exec / 1e12:.3f} TFLOP executed per launch "
                                     f"(4*B*d*sum(mask*len) + 4*T_t*T*d)"},
@@ -536,17 +694,39 @@ def run_ours(args):
         }
     if not args.profile:
         line["clocks"] = clocks.summary()
+    if world == 1 and not args.no_extras and not args.profile and args.config == "hv":
+        line["extras"] = extras(torch, nat, lib, workspace_for, args, q, k, v, out, ws, dev, peaks["bf16"])
     if world == 1 and not args.no_cpu_baseline and not args.profile:
-        cb = cpu_reference_sample(cfg, f, args.variant, args.cpu_sample_blocks)
-        line["cpu_baseline"] = {"value": cb["ms_per_call"], "unit": "ms/call", "cores": cb["cores"],
-                                "kind": "port", "sample": cb["sample"], "sample_s": cb["sample_s"]}
+        res = cpu_heads(args, args.cpu_heads, args.cpu_warmup)
+        per_head = statistics.median(res["head_s"])
+        line["cpu_baseline"] = {"value": per_head * cfg["heads"] * 1e3, "unit": "ms/call", "cores": res["cores"],
+                                "kind": res["kind"], "sample": cpu_sample_text(res, cfg["heads"]),
+                                "env": res["env"], "cpu_model": cpu_model(), "per_head_s": per_head}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
+def spawn_ranks(args) -> bool:
+    """`--gpus N` (N > 1) outside torchrun: re-launch this command as N ranks
+    (torch.distributed.run, 127.0.0.1 rendezvous); rank 0 prints the line."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ or args.cpu_worker:
+        return False
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    sys.exit(subprocess.run(cmd).returncode)
+
+
 def main():
     args = parse()
+    if args.cpu_worker:
+        cpu_worker(args)
+        return
+    spawn_ranks(args)
     if args.impl == "reference":
         run_reference(args)
     else:

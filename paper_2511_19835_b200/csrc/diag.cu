@@ -10,7 +10,6 @@
 // Needs rsa_pool + rsa_select on the workspace (pooled scores, deficits).
 #include "rsa_internal.cuh"
 
-#include <cublas_v2.h>
 
 #include <algorithm>
 #include <cfloat>
@@ -171,14 +170,6 @@ __global__ void __launch_bounds__(DT) softmax_rows_kernel(double* __restrict__ S
   for (int64_t j = threadIdx.x; j < T; j += DT) row[j] = row[j] / sum;
 }
 
-cublasHandle_t diag_cublas() {
-  static thread_local cublasHandle_t handles[64] = {};
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-  if (!handles[dev] && cublasCreate(&handles[dev]) != CUBLAS_STATUS_SUCCESS) handles[dev] = nullptr;
-  return handles[dev];
-}
-
 }  // namespace
 
 int64_t diag_chunk_blocks(const Geometry& g) {
@@ -194,8 +185,6 @@ size_t diag_scratch_size(const Geometry& g) {
 cudaError_t launch_diagnostics(const Geometry& g, const void* q, const void* k, const Workspace& ws,
                                double* gain, double* error, double* exact_gain, double* exact_error,
                                double* s_sum, double* s_sum_pool, void* scratch, cudaStream_t st) {
-  cublasHandle_t hb = diag_cublas();
-  if (!hb || cublasSetStream(hb, st) != CUBLAS_STATUS_SUCCESS) return cudaErrorInitializationError;
   const int64_t nc = diag_chunk_blocks(g);
   double* k64 = static_cast<double*>(scratch);
   double* q64 = k64 + g.T * g.d;
@@ -218,11 +207,9 @@ cudaError_t launch_diagnostics(const Geometry& g, const void* q, const void* k, 
     diag_pooled_kernel<<<(unsigned)g.N, DT, 0, st>>>(ws, g, h, a_tok, exact_gain, gain, error, pmax, 1.0 / sqrt_d);
     for (int64_t n0 = 0; n0 < g.N; n0 += nc) {
       const int64_t cn = std::min(nc, g.N - n0), rows = cn * g.B;
-      const double one = 1.0, zero = 0.0;
-      // S (row-major rows x T) = q64[rows] . k64^T  (column-major T x rows)
-      if (cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, (int)g.T, (int)rows, (int)g.d, &one, k64, (int)g.d,
-                      q64 + n0 * g.B * g.d, (int)g.d, &zero, S, (int)g.T) != CUBLAS_STATUS_SUCCESS)
-        return cudaErrorUnknown;
+      // S (row-major rows x T) = q64[rows] . k64^T
+      cudaError_t e = launch_dgemm(1, rows, g.T, g.d, q64 + n0 * g.B * g.d, g.d, 0, k64, g.d, 0, true, S, g.T, 0, st);
+      if (e != cudaSuccess) return e;
       diag_row_kernel<<<(unsigned)rows, DT, 0, st>>>(S, ws, g, h, n0 * g.B, pmax, rmax, rsum, s_sum, s_sum_pool,
                                                       sqrt_d);
       diag_err_kernel<<<dim3((unsigned)g.M, (unsigned)cn), DT, 0, st>>>(S, g, h, n0, rmax, rsum, a_tok,
@@ -241,8 +228,6 @@ size_t dense_scratch_size(const Geometry& g) {
 // the reference's ground truth full_attention_oracle (core.py:211-225).
 cudaError_t launch_dense_reference(const Geometry& g, const void* q, const void* k, const void* v, double* out,
                                    void* scratch, cudaStream_t st) {
-  cublasHandle_t hb = diag_cublas();
-  if (!hb || cublasSetStream(hb, st) != CUBLAS_STATUS_SUCCESS) return cudaErrorInitializationError;
   const int64_t rows_per = diag_chunk_blocks(g) * g.B;
   double* k64 = static_cast<double*>(scratch);
   double* v64 = k64 + g.T * g.d;
@@ -263,15 +248,13 @@ cudaError_t launch_dense_reference(const Geometry& g, const void* q, const void*
     convert(static_cast<const char*>(q) + off, q64, g.T * g.d);
     for (int64_t r0 = 0; r0 < g.T; r0 += rows_per) {
       const int64_t rows = std::min(rows_per, g.T - r0);
-      const double one = 1.0, zero = 0.0;
-      if (cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, (int)g.T, (int)rows, (int)g.d, &one, k64, (int)g.d,
-                      q64 + r0 * g.d, (int)g.d, &zero, W, (int)g.T) != CUBLAS_STATUS_SUCCESS)
-        return cudaErrorUnknown;
+      // W (row-major rows x T) = q64[rows] . k64^T
+      cudaError_t e = launch_dgemm(1, rows, g.T, g.d, q64 + r0 * g.d, g.d, 0, k64, g.d, 0, true, W, g.T, 0, st);
+      if (e != cudaSuccess) return e;
       softmax_rows_kernel<<<(unsigned)rows, DT, 0, st>>>(W, g.T, sqrt_d);
       // out rows (row-major rows x d) = W (rows x T) . V (T x d)
-      if (cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)g.d, (int)rows, (int)g.T, &one, v64, (int)g.d, W,
-                      (int)g.T, &zero, out + (h * g.T + r0) * g.d, (int)g.d) != CUBLAS_STATUS_SUCCESS)
-        return cudaErrorUnknown;
+      e = launch_dgemm(1, rows, g.d, g.T, W, g.T, 0, v64, g.d, 0, false, out + (h * g.T + r0) * g.d, g.d, 0, st);
+      if (e != cudaSuccess) return e;
     }
   }
   return cudaGetLastError();

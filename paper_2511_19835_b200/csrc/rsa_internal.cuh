@@ -99,6 +99,11 @@ cudaError_t launch_pool(const Geometry& g, const void* q, const void* k, const v
                         const Workspace& ws, cudaStream_t st, int* launches,
                         const int32_t* perm = nullptr, void* kp = nullptr, void* vp = nullptr,
                         void* qp = nullptr);
+// fp64 DMMA GEMM (gemm_f64.cu): C[b] = A[b] . op(B[b]), row-major,
+// op(B) = B^T (B is N x K) when b_transposed, else B (K x N)
+cudaError_t launch_dgemm(int64_t batch, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                         int64_t strideA, const double* B, int64_t ldb, int64_t strideB, bool b_transposed,
+                         double* C, int64_t ldc, int64_t strideC, cudaStream_t st);
 cudaError_t launch_select(const Geometry& g, const rsa_config& cfg, int64_t k_floor,
                           const Workspace& ws, cudaStream_t st, int* launches);
 cudaError_t launch_lists_from_mask(const Geometry& g, const uint8_t* mask,

@@ -22,7 +22,6 @@
 // numpy's stable argsort of -a_pool.
 #include "rsa_internal.cuh"
 
-#include <cublas_v2.h>
 
 #include <algorithm>
 #include <cfloat>
@@ -845,32 +844,17 @@ __global__ void tile_lists_kernel(Workspace ws, Geometry g) {
   if (lane == 0) ws.tile_count[h * tiles_per_head + t] = count;
 }
 
-// one cuBLAS handle per host thread and device (the fp64 GEMMs of K2)
-cublasHandle_t cublas_handle() {
-  static thread_local cublasHandle_t handles[64] = {};
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-  if (!handles[dev] && cublasCreate(&handles[dev]) != CUBLAS_STATUS_SUCCESS) handles[dev] = nullptr;
-  return handles[dev];
-}
-
 }  // namespace
 
 cudaError_t launch_select(const Geometry& g, const rsa_config& cfg, int64_t k_floor,
                           const Workspace& ws, cudaStream_t st, int* launches) {
   const double sqrt_d = sqrt((double)g.d);
-  // scores = q_pool @ k_cat^T (select_rows divides by sqrt(d)): a plain
-  // strided-batched fp64 GEMM, row-major [N][n_cols] = column-major n_cols x N
-  cublasHandle_t hb = cublas_handle();
-  if (!hb) return cudaErrorInitializationError;
-  if (cublasSetStream(hb, st) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
-  {
-    const double one = 1.0, zero = 0.0;
-    if (cublasDgemmStridedBatched(hb, CUBLAS_OP_T, CUBLAS_OP_N, (int)g.n_cols, (int)g.N, (int)g.d, &one,
-                                  ws.k_cat, (int)g.d, g.n_cols * g.d, ws.q_pool, (int)g.d, g.N * g.d, &zero,
-                                  ws.scores, (int)g.n_cols, g.N * g.n_cols, (int)g.H) != CUBLAS_STATUS_SUCCESS)
-      return cudaErrorUnknown;   // library kernel: not counted in *launches (ours only)
-  }
+  // scores = q_pool @ k_cat^T (select_rows divides by sqrt(d), ipar.py:41):
+  // [N][n_cols] per head, our DMMA GEMM
+  cudaError_t e = launch_dgemm(g.H, g.N, g.n_cols, g.d, ws.q_pool, g.d, g.N * g.d, ws.k_cat, g.d,
+                               g.n_cols * g.d, true, ws.scores, g.n_cols, g.N * g.n_cols, st);
+  if (e != cudaSuccess) return e;
+  ++*launches;
   SelectParams P;
   P.g = g;
   P.ws = ws;
@@ -903,7 +887,6 @@ cudaError_t launch_select(const Geometry& g, const rsa_config& cfg, int64_t k_fl
       kern<<<dim3((unsigned)g.N, (unsigned)g.H), RT, smem, st>>>(P);
       return cudaSuccess;
     };
-    cudaError_t e;
     if (cum)
       e = per <= 4 ? launch(select_rows_reg_kernel<4, true>)
         : per <= 8 ? launch(select_rows_reg_kernel<8, true>)
@@ -928,15 +911,12 @@ cudaError_t launch_select(const Geometry& g, const rsa_config& cfg, int64_t k_fl
     select_rows_kernel<<<dim3((unsigned)g.N, (unsigned)g.H), RT, smem, st>>>(P);
   }
   ++*launches;
-  // compensation rows: (a_pool masked to applied) @ v_pool   (rectify.py:84-87);
-  // select_rows wrote the masked operand.  Row-major [N][d] = col-major d x N
-  {
-    const double one = 1.0, zero = 0.0;
-    if (cublasDgemmStridedBatched(hb, CUBLAS_OP_N, CUBLAS_OP_N, (int)g.d, (int)g.N, (int)g.M, &one,
-                                  ws.v_pool, (int)g.d, g.M * g.d, ws.a_applied, (int)g.M, g.N * g.M, &zero,
-                                  ws.comp, (int)g.d, g.N * g.d, (int)g.H) != CUBLAS_STATUS_SUCCESS)
-      return cudaErrorUnknown;   // library kernel: not counted in *launches (ours only)
-  }
+  // compensation rows: (a_pool masked to applied) @ v_pool (rectify.py:84-87);
+  // select_rows wrote the masked operand.  [N][d] per head
+  e = launch_dgemm(g.H, g.N, g.d, g.M, ws.a_applied, g.M, g.N * g.M, ws.v_pool, g.d, g.M * g.d, false,
+                   ws.comp, g.d, g.N * g.d, st);
+  if (e != cudaSuccess) return e;
+  ++*launches;
   return cudaGetLastError();
 }
 

@@ -56,9 +56,12 @@ def head_parallel_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *
     sizes = [head_range(q.shape[1], world, r) for r in range(world)]
     if len({h - l for l, h in sizes}) != 1:
         raise ValueError("gather needs equal head shards (H divisible by the world size)")
-    parts = [torch.empty_like(out) for _ in range(world)]
-    dist.all_gather(parts, out.contiguous(), group=group)
-    return torch.cat(parts, dim=1)
+    staged = dist.get_backend(group) != "nccl" and out.device.type != "cpu"   # gloo: host staging
+    src = out.contiguous().cpu() if staged else out.contiguous()
+    parts = [torch.empty_like(src) for _ in range(world)]
+    dist.all_gather(parts, src, group=group)
+    full = torch.cat(parts, dim=1)
+    return full.to(out.device) if staged else full
 
 
 def seq_to_head(x: torch.Tensor, group=None) -> torch.Tensor:
@@ -90,27 +93,96 @@ def head_to_seq(x: torch.Tensor, group=None) -> torch.Tensor:
     return recv.permute(1, 0, 2, 3, 4).reshape(b, world * hp, s_loc, d)
 
 
+def _a2a(recvs: list, sends: list, group, nccl: bool):
+    """All-to-all of one head: ``sends[p]`` goes to rank p, rank p's piece
+    lands in ``recvs[p]`` (contiguous [S/P, d] views, written in place).
+    NCCL: list all-to-all (grouped ncclSend/ncclRecv, no staging copies),
+    asynchronous on the process group's stream.  gloo (CPU tests, and the
+    one-GPU plumbing run) only has the flat all_to_all_single: the sends are
+    packed, CUDA tensors staged through host memory, synchronously."""
+    if nccl:
+        return dist.all_to_all(recvs, sends, group=group, async_op=True)
+    packed = torch.stack(sends)
+    packed = packed.cpu() if packed.device.type != "cpu" else packed
+    got = torch.empty_like(packed)
+    dist.all_to_all_single(got, packed, group=group)
+    for p, r in enumerate(recvs):
+        r.copy_(got[p])
+    return None
+
+
 def ulysses_attention(q_video: torch.Tensor, k_video: torch.Tensor, v_video: torch.Tensor,
                       q_text: torch.Tensor, k_text: torch.Tensor, v_text: torch.Tensor, *,
-                      group=None, attn_fn: Callable | None = None, **kw):
+                      group=None, attn_fn: Callable | None = None, heads_per_group: int = 1, **kw):
     """Rectified sparse attention on sequence-sharded video tokens.
 
     q/k/v_video: [B, H, T_v/P, d] (this rank's contiguous slice of the video
     tokens); q/k/v_text: [B, H, T_t, d] replicated.  Returns
-    (o_video [B, H, T_v/P, d], o_text [B, H, T_t, d] replicated)."""
+    (o_video [B, H, T_v/P, d], o_text [B, H, T_t, d] replicated).
+
+    This rank's H/P heads run in groups of ``heads_per_group``: every input
+    all-to-all is queued up front on the communication stream and group g's
+    attention waits only for its own heads, so the shuffle of group g+1 (and
+    the output shuffle of group g-1) overlaps group g's K1 -> K2 -> K3.  Each
+    head's pieces are received straight into a preallocated [B, H/P, T, d]
+    buffer whose text rows are filled once, and the attention writes into an
+    output buffer the return shuffle reads in place -- no concatenation or
+    permute copies (the send side reads strided per-head views)."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     fn = attn_fn or _attention
-    t_t = q_text.shape[2]
-    h = q_video.shape[1]
+    b, h, s_loc, d = q_video.shape
+    if h % world:
+        raise ValueError(f"heads ({h}) must be divisible by the world size ({world})")
     hp = h // world
+    t_t = q_text.shape[2]
+    t_v = s_loc * world
+    T = t_v + t_t
+    nccl = dist.get_backend(group) == "nccl"
     lo, hi = rank * hp, (rank + 1) * hp
-    q = torch.cat([seq_to_head(q_video, group), q_text[:, lo:hi]], dim=2).contiguous()
-    k = torch.cat([seq_to_head(k_video, group), k_text[:, lo:hi]], dim=2).contiguous()
-    v = torch.cat([seq_to_head(v_video, group), v_text[:, lo:hi]], dim=2).contiguous()
-    out = fn(q, k, v, t_t, **kw)                         # [B, H/P, T_v + T_t, d]
-    t_v = out.shape[2] - t_t
-    o_video = head_to_seq(out[:, :, :t_v].contiguous(), group)
-    parts = [torch.empty_like(out[:, :, t_v:].contiguous()) for _ in range(world)]
-    dist.all_gather(parts, out[:, :, t_v:].contiguous(), group=group)
-    return o_video, torch.cat(parts, dim=1)
+    videos = (q_video, k_video, v_video)
+    bufs = []
+    for x, xt in zip(videos, (q_text, k_text, v_text)):
+        buf = x.new_empty(b, hp, T, d)
+        buf[:, :, t_v:] = xt[:, lo:hi]
+        bufs.append(buf)
+    groups = [(g0, min(hp, g0 + max(1, heads_per_group))) for g0 in range(0, hp, max(1, heads_per_group))]
+
+    def shuffle_in(g0, g1):
+        works = []
+        for x, buf in zip(videos, bufs):
+            for bi in range(b):
+                for hl in range(g0, g1):
+                    # rank p's slice of my head lo + hl -> rows [p S/P, (p+1) S/P) of my buffer
+                    works.append(_a2a(list(buf[bi, hl, :t_v].chunk(world)),
+                                      [x[bi, p * hp + hl] for p in range(world)], group, nccl))
+        return [w for w in works if w is not None]
+
+    pending = [shuffle_in(g0, g1) for g0, g1 in groups]
+    obuf = q_video.new_empty(b, hp, T, d)
+    o_video = q_video.new_empty(b, h, s_loc, d)
+    out_works = []
+    for (g0, g1), works in zip(groups, pending):
+        for w in works:
+            w.wait()                      # the compute stream waits for this group's heads only
+        args = (bufs[0][:, g0:g1], bufs[1][:, g0:g1], bufs[2][:, g0:g1])
+        if attn_fn is None and b == 1:
+            fn(*args, t_t, out=obuf[:, g0:g1], **kw)
+        else:
+            obuf[:, g0:g1] = fn(*(a.contiguous() for a in args), t_t, **kw)
+        for bi in range(b):
+            for hl in range(g0, g1):
+                # sequence slice p of my head lo + hl -> rank p; rank p's head p hp + hl -> my slice
+                w = _a2a([o_video[bi, p * hp + hl] for p in range(world)],
+                         list(obuf[bi, hl, :t_v].chunk(world)), group, nccl)
+                if w is not None:
+                    out_works.append(w)
+    text = obuf[:, :, t_v:].contiguous()
+    staged = not nccl and text.device.type != "cpu"   # gloo: host staging
+    src = text.cpu() if staged else text
+    parts = [torch.empty_like(src) for _ in range(world)]
+    dist.all_gather(parts, src, group=group)
+    o_text = torch.cat(parts, dim=1)
+    for w in out_works:
+        w.wait()
+    return o_video, (o_text.to(text.device) if staged else o_text)

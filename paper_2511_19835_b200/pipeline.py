@@ -277,7 +277,7 @@ def rectified_sparse_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor
                                check_status: bool = True, status: torch.Tensor | None = None,
                                heads_per_chunk: int = 1,
                                grid_dims: tuple | None = None, morton: bool = False,
-                               ragged_video: bool = False) -> torch.Tensor:
+                               ragged_video: bool = False, out: torch.Tensor | None = None) -> torch.Tensor:
     """Rectified block-sparse attention for every (batch, head) of q/k/v
     ([..., T, d], the last ``num_text_tokens`` rows text).  ``sparsity=s`` is
     shorthand for top_k_fraction = 1 - s with p = 0, r = 0, no forced text.
@@ -301,7 +301,9 @@ def rectified_sparse_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor
     output stay in the original token order.
     ``ragged_video=True`` accepts a video token count that is not a multiple of
     ``block`` (the final video block is shorter; an extension -- the reference
-    raises BlockSizeError), e.g. HunyuanVideo's exact 118,800 tokens."""
+    raises BlockSizeError), e.g. HunyuanVideo's exact 118,800 tokens.
+    ``out`` (CUDA tensors): a contiguous tensor of q's shape and dtype the
+    result is written into (e.g. a slice of a caller's buffer)."""
     if sparsity is not None:
         top_k_fraction, weight_threshold, adjacency_radius, force_text_blocks = 1.0 - sparsity, 0.0, 0, False
     if top_k_fraction is None:
@@ -333,9 +335,14 @@ def rectified_sparse_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor
         t, hh, w = grid_dims
         if t * hh * w != T - t_t:
             raise ShapeError(f"grid_dims product {t * hh * w} != T_v={T - t_t}")
+        if out is not None:
+            raise ShapeError("out= is not supported with morton=True")
         out = permuted_forward(q, k, v, shape, cfg, device_permutation(grid_dims, q.device), lse, workspace)
     else:
-        out = torch.empty_like(q)
+        if out is None:
+            out = torch.empty_like(q)
+        elif out.shape != q.shape or out.dtype != q.dtype or out.device != q.device or not out.is_contiguous():
+            raise ShapeError(f"out must be a contiguous {q.dtype} tensor of shape {tuple(q.shape)} on {q.device}")
         nat.check(nat.lib().rsa_forward(C.byref(shape), C.byref(cfg), _ptr(q), _ptr(k), _ptr(v),
                                         _ptr(out), _ptr(lse), _ptr(workspace), _stream()))
     _report_status(workspace, status, check_status)

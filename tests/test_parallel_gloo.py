@@ -90,6 +90,21 @@ def check_ulysses_matches_single_process(rank, _q):
     torch.testing.assert_close(o_text, full[:, :, qv.shape[2]:], rtol=0, atol=0)
 
 
+def check_ulysses_grouped_batched(rank, _q):
+    """Two batch entries, head groups of 2 (each group's shuffle overlaps the
+    previous group's attention on NCCL; here the same data movement, gloo)."""
+    qv, qt, kv, kt, vv, vt = _problem(seed=4, b=2, h=4)
+    s_loc = qv.shape[2] // WORLD
+    sl = slice(rank * s_loc, (rank + 1) * s_loc)
+    for hpg in (1, 2):
+        o_video, o_text = ulysses_attention(qv[:, :, sl].contiguous(), kv[:, :, sl].contiguous(),
+                                            vv[:, :, sl].contiguous(), qt, kt, vt, attn_fn=oracle_attn,
+                                            heads_per_group=hpg)
+        full = oracle_attn(torch.cat([qv, qt], 2), torch.cat([kv, kt], 2), torch.cat([vv, vt], 2), qt.shape[2])
+        torch.testing.assert_close(o_video, full[:, :, :qv.shape[2]][:, :, sl], rtol=0, atol=0)
+        torch.testing.assert_close(o_text, full[:, :, qv.shape[2]:], rtol=0, atol=0)
+
+
 def check_head_parallel_gather(rank, _q):
     qv, qt, kv, kt, vv, vt = _problem(seed=5)
     q, k, v = torch.cat([qv, qt], 2), torch.cat([kv, kt], 2), torch.cat([vv, vt], 2)
@@ -104,6 +119,6 @@ def test_head_range_balanced():
 
 
 @pytest.mark.parametrize("fn", ["check_shuffle_roundtrip", "check_ulysses_matches_single_process",
-                                "check_head_parallel_gather"])
+                                "check_ulysses_grouped_batched", "check_head_parallel_gather"])
 def test_gloo_world2(fn):
     _run(fn)
