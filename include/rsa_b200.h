@@ -52,7 +52,17 @@ typedef enum {
  * block/head_dim in {64,128} (the two-tile ping-pong kernel at block = head_dim
  * = 128, the persistent one-tile kernel otherwise), the CUDA-core kernel for
  * everything else (fp32/fp64, other block sizes). */
-typedef enum { RSA_KERNEL_AUTO = 0, RSA_KERNEL_TCGEN05 = 1, RSA_KERNEL_SIMT = 2 } rsa_kernel;
+/* AUTO: bf16 -> the tcgen05 kernel of the shape class (d = B = 128: the
+ * two-tile ping-pong kernel; else the one-tile persistent kernel), f32/f64 ->
+ * the CUDA-core kernel.  TCGEN05_PERSISTENT forces the one-tile persistent
+ * tcgen05 kernel at d = B = 128 and SIMT the CUDA-core kernel for bf16
+ * (cross-checks; never chosen silently). */
+typedef enum {
+  RSA_KERNEL_AUTO = 0,
+  RSA_KERNEL_TCGEN05 = 1,
+  RSA_KERNEL_SIMT = 2,
+  RSA_KERNEL_TCGEN05_PERSISTENT = 3
+} rsa_kernel;
 
 /* rsa_shape.flags */
 #define RSA_SHAPE_RAGGED_VIDEO 1  /* allow T_v % block != 0: the final video block holds

@@ -6,24 +6,17 @@
 // an online softmax over the retained kv blocks in ascending order -- and
 // apply_rectification (rectify.py:66-89): O' = R_n O + sum_applied a_pool v_pool.
 //
-// One CTA = one 128-row query tile (UMMA M = 128): one video query block for
-// B = 128, two for B = 64 (walking the union of their kv lists with per-row
-// membership), or 128 text queries (every kv block).  Warp roles:
-//   warp 0      TMA producer: Q once, then K_j / V_j tiles (box 64 x B, 128B
-//               swizzle) into an NST-stage ring in exactly the order the MMA
-//               warp consumes them (K0 K1 V0 K2 V1 ... V_{c-1})
-//   warp 1      single-thread tcgen05.mma issuer:
-//                 S_j = Q K_j^T  (SS, into TMEM S buffer j%2)   -- issued one
-//                 step ahead, so it runs while softmax works on S_{j-1}
-//                 O  += P_j V_j  (TS: P_j read straight from TMEM)
-//   warp 2      TMEM allocation / release
-//   warps 4-11  softmax: two threads per query row (TMEM lane), each owning
-//               half of the score columns; fp32 online softmax in the log2 domain with lazy (threshold 2^8) O
-//               rescaling, P packed to bf16 back into the S columns; then the
-//               epilogue O / l * R_n + comp_n -> bf16 store, LSE.
-// TMEM columns: S0 [0,B), S1 [B,2B), O [2B, 2B+D).
+// Two kernels, one per shape class:
+//   attn_tc_pp_kernel          d = B = 128 (HunyuanVideo, Wan): two query tiles
+//                              per CTA in independent ping-pong slots
+//   attn_tc_persistent_kernel  B = 64 and/or d = 64 (and on request for
+//                              d = B = 128): one query tile at a time per CTA
+// Both are persistent (one CTA per SM) and walk 128-row query tiles head-major:
+// video tiles over their kv lists, text tiles over every kv block in split-K
+// chunks that text_combine_kernel merges.
 #include "rsa_internal.cuh"
 #include "tc_ptx.cuh"
+#include "tmap.cuh"
 
 #include <cuda.h>
 #include <algorithm>
@@ -37,29 +30,24 @@ constexpr int kThreads = 384;   // 4 control warps + 8 softmax warps
 constexpr float kRescaleThreshold = 12.0f;  // log2 units: rescale O only if the row max grows by > 2^12
                                             // (P <= 2^12 stays exact-range in bf16 / fp32; 8 measured ~1 % slower)
 
-template <int D, int BKV, bool QTM, bool VT>
+// persistent kernel: Q resident in TMEM (A operand of the S MMAs), two S/P
+// TMEM buffers, a K/V ring of NST stages in shared memory
+template <int D, int BKV>
 struct Cfg {
-  // S/P TMEM buffers: 3 when Q stays in shared memory, so S_{j+1} never
-  // overwrites the buffer PV_{j-1} is still reading (a TMEM WAR hazard that
-  // drains the tensor pipe every step); 2 when Q lives in TMEM
-  static constexpr int NS = QTM ? 2 : 3;
-  // K/V ring depth: Q in TMEM frees its 32 KB of shared memory for 2 more stages
-  static constexpr int NST = BKV * D * 2 <= 16384 ? 8 : (QTM ? 6 : 5);
+  static constexpr int NS = 2;
+  static constexpr int NST = BKV * D * 2 <= 16384 ? 8 : 6;
   static constexpr int PANELS = D / 64;
   static constexpr int Q_PANEL = 128 * 128;     // bytes: 128 rows x 128 B
   static constexpr int KV_PANEL = BKV * 128;    // bytes: B rows x 128 B
   static constexpr int Q_BYTES = 128 * D * 2;
   static constexpr int STAGE = BKV * D * 2;
   static constexpr int O_COL = NS * BKV;
-  static constexpr int Q_COL = NS * BKV + D;      // Q (bf16 pairs) when resident in TMEM
-  static constexpr int TMEM_USED = NS * BKV + D + (QTM ? D / 2 : 0);
+  static constexpr int Q_COL = NS * BKV + D;      // Q (bf16 pairs) resident in TMEM
+  static constexpr int TMEM_USED = NS * BKV + D + D / 2;
   static constexpr int TMEM_COLS = TMEM_USED <= 256 ? 256 : 512;
-  static constexpr int Q_SMEM = QTM ? 0 : Q_BYTES;
-  static constexpr int SMEM = 1024 + Q_SMEM + NST * STAGE + 256 + 768 * 4;
+  static constexpr int SMEM = 1024 + NST * STAGE + 256 + 768 * 4;
   static constexpr uint32_t IDESC_S = ptx::idesc_bf16(128, BKV, false);
-  // PV B operand: V^T tiles (K-major) or V tiles (MN-major)
-  static constexpr uint32_t IDESC_O = ptx::idesc_bf16(128, D, !VT);
-  static constexpr int VT_PANEL = D * 128;      // bytes: D rows (head dims) x 128 B (64 keys)
+  static constexpr uint32_t IDESC_O = ptx::idesc_bf16(128, D, true);   // PV B operand: V tiles (MN-major)
 };
 
 struct TcParams {
@@ -78,444 +66,9 @@ struct TcParams {
   int64_t video_tiles_per_head;
   int64_t tiles_per_head;        // text_tiles_per_head * text_chunks + video_tiles_per_head
   float scale_log2;  // log2(e) / sqrt(d)
-  int trace_cta;     // CTA traced per step when stamps == 2
-  int stamps;        // RSA_TC_STAMPS=1: per-CTA globaltimer stamps into `lse` (profiling)
   int qring;         // persistent kernel: each tile's Q rows arrive by TMA in a K/V ring stage
-  int pp_lock;       // ping-pong kernel: each MMA group + commits issued under a CTA lock
-  int mma_spin;      // persistent kernel: the MMA warp polls P (no try_wait suspend)
-  int sm_spin;       // persistent kernel: the softmax warps poll S
-  int mode;          // 0 normal; diagnostics: 1 no softmax math, 2 TMA only, 3 MMA only, 4 MMA+TMA,
-                     // 6 softmax only, 7 normal + per-CTA globaltimer stamps into `lse`
 };
 
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-
-template <int D, int BKV, bool QTM, bool VT, int EMU>
-__global__ void __launch_bounds__(kThreads, 1)
-attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-               const __grid_constant__ CUtensorMap tm_v, const TcParams P) {
-  using C = Cfg<D, BKV, QTM, VT>;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* q_s = base;
-  uint8_t* kv_s = base + C::Q_SMEM;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(kv_s + C::NST * C::STAGE);
-  uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;
-  uint64_t* kv_empty = kv_full + C::NST;
-  uint64_t* s_full = kv_empty + C::NST;    // [NS]
-  uint64_t* p_full = s_full + C::NS;       // [NS]
-  uint64_t* pv_done = p_full + C::NS;      // [1]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 1);
-  float* red_max = reinterpret_cast<float*>(bars + 32);   // [2][2][128] row maxima + [2][128] row sums
-
-  const Geometry& g = P.g;
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  unsigned long long* tstamp =
-      (P.stamps && P.lse) ? reinterpret_cast<unsigned long long*>(P.lse) + blockIdx.x * 8 : nullptr;
-  // per-step clock64 trace of one CTA (P.stamps == 2): [step][8] after the per-CTA stamps
-  long long* trace = (P.stamps == 2 && P.lse && blockIdx.x == (unsigned)P.trace_cta)
-                         ? reinterpret_cast<long long*>(P.lse) + (int64_t)gridDim.x * 8 : nullptr;
-  if (tstamp && threadIdx.x == 0) {
-    tstamp[0] = gtimer();
-    uint32_t smid;
-    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-    tstamp[7] = smid;
-  }
-
-  // ---- tile decode: head-major, each head's text chunks first, then its
-  // video tiles, so the K/V blocks of ~one head are in flight at a time (L2).
-  // A text tile walks every kv block; it is split into `text_chunks` chunks of
-  // `chunk_blocks` blocks whose partial (O, m, l) text_combine_kernel merges.
-  const int64_t bid = blockIdx.x;
-  const int64_t h = bid / P.tiles_per_head;
-  const int64_t r_in = bid % P.tiles_per_head;
-  const int64_t n_text_ct = P.text_tiles_per_head * P.text_chunks;
-  const bool text = r_in < n_text_ct;
-  int64_t q_row0, rows_valid, count, m_first = 0, part = 0;
-  const int32_t* list = nullptr;
-  if (text) {
-    const int64_t t = r_in / P.text_chunks, c = r_in % P.text_chunks;
-    q_row0 = g.Tv + t * 128;
-    rows_valid = min((int64_t)128, g.Tt - t * 128);
-    m_first = c * P.chunk_blocks;
-    count = min(g.M, m_first + P.chunk_blocks) - m_first;
-    part = (h * P.text_tiles_per_head + t) * P.text_chunks + c;
-  } else {
-    const int64_t t = r_in - n_text_ct;
-    q_row0 = t * 128;
-    rows_valid = min((int64_t)128, g.Tv - q_row0);
-    if (g.B == 128) {   // one query block per tile: its own kv list (tile_lists skipped)
-      count = P.ws.kv_count[h * g.N + t];
-      list = P.ws.kv_list + (h * g.N + t) * g.M;
-    } else {
-      count = P.ws.tile_count[h * P.video_tiles_per_head + t];
-      list = P.ws.tile_list + (h * P.video_tiles_per_head + t) * g.M;
-    }
-  }
-
-  if (threadIdx.x == 0) {
-    ptx::mbar_init(q_full, QTM ? 256 : 1);
-    for (int i = 0; i < C::NST; ++i) {
-      ptx::mbar_init(kv_full + i, 1);
-      ptx::mbar_init(kv_empty + i, 1);
-    }
-    for (int i = 0; i < C::NS; ++i) {
-      ptx::mbar_init(s_full + i, 1);
-      ptx::mbar_init(p_full + i, 256);
-    }
-    ptx::mbar_init(pv_done, 1);
-    ptx::fence_barrier_init();
-  }
-  if (warp == 2) ptx::tmem_alloc<C::TMEM_COLS>(tmem_slot);
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  if (tstamp && threadIdx.x == 0) tstamp[1] = gtimer();
-
-  if (warp == 0) {
-    // ===================== TMA producer =====================
-    if (lane == 0 && count > 0 && P.mode != 3 && P.mode != 6) {
-      ptx::prefetch_tmap(&tm_q);
-      ptx::prefetch_tmap(&tm_k);
-      ptx::prefetch_tmap(&tm_v);
-      if (!QTM) {
-        ptx::mbar_expect_tx(q_full, C::Q_BYTES);
-#pragma unroll
-        for (int p = 0; p < C::PANELS; ++p)
-          ptx::tma_load_3d(q_s + p * C::Q_PANEL, &tm_q, q_full, 64 * p, (int)q_row0, (int)h);
-      }
-      int it = 0;
-      const uint64_t keep = ptx::policy_evict_last();   // K/V blocks are re-read by many tiles of the head
-      auto load = [&](int64_t j, bool is_v) {
-        const int s = it % C::NST;
-        const uint32_t ph = (it / C::NST) & 1;
-        const int64_t m = list ? (list[j] & 0xFFFFFF) : m_first + j;
-        ptx::mbar_wait(kv_empty + s, ph ^ 1);
-        if (trace && j < 64) trace[j * 8 + (is_v ? 7 : 6)] = clock64();
-        ptx::mbar_expect_tx(kv_full + s, C::STAGE);
-        uint8_t* dst = kv_s + s * C::STAGE;
-        const int panels = (is_v && VT) ? BKV / 64 : C::PANELS;
-        for (int p = 0; p < panels; ++p)
-          if (is_v && VT)   // V^T: box (64 keys, D dims) per 64-key panel
-            ptx::tma_load_3d_hint(dst + p * C::VT_PANEL, &tm_v, kv_full + s, (int)kv_row0(g, m) + 64 * p, 0, (int)h, keep);
-          else if (is_v)    // V: box (64 dims, B keys) per 64-dim panel
-            ptx::tma_load_3d_hint(dst + p * C::KV_PANEL, &tm_v, kv_full + s, 64 * p, (int)kv_row0(g, m), (int)h, keep);
-          else
-            ptx::tma_load_3d_hint(dst + p * C::KV_PANEL, &tm_k, kv_full + s, 64 * p, (int)kv_row0(g, m), (int)h, keep);
-        ++it;
-      };
-      for (int64_t j = 0; j <= count; ++j) {
-        if (j < count) load(j, false);
-        if (j >= 1) load(j - 1, true);
-      }
-    }
-  } else if (warp == 1) {
-    // ===================== MMA issuer =====================
-    if (P.mode == 6 || P.mode == 2) {
-      if (lane == 0 && count > 0 && P.mode == 6) {
-      // diagnostic: softmax alone -- hand out S buffers without any MMA
-      for (int64_t j = 0; j < count; ++j) {
-        if (j >= 1) {
-          ptx::mbar_wait(p_full + ((j - 1) % C::NS), (uint32_t)(((j - 1) / C::NS) & 1));
-          ptx::tc_commit(pv_done);          // "PV_{j-1}" done: one phase per step
-        }
-        ptx::tc_commit(s_full + (j % C::NS));
-      }
-      ptx::mbar_wait(p_full + ((count - 1) % C::NS), (uint32_t)(((count - 1) / C::NS) & 1));
-      ptx::tc_commit(pv_done);
-      } else if (lane == 0 && count > 0) {
-      // diagnostic: consume the K/V stream without any MMA (TMA rate only)
-      for (int it = 0; it < 2 * count; ++it) {
-        ptx::mbar_wait(kv_full + it % C::NST, (it / C::NST) & 1);
-        ptx::mbar_arrive(kv_empty + it % C::NST);
-      }
-      }
-    } else if (count > 0) {
-      // The whole warp runs the issue loop (converged, warp-uniform
-      // descriptors in uniform registers); one elected lane issues each
-      // tcgen05.mma / commit.  Lane-0-only code made the compiler wrap every
-      // UTCHMMA in an ELECT/R2UR.BROADCAST waterfall (~15 instr, profiles/r01a).
-      ptx::mbar_wait(q_full, 0);
-      ptx::tc_fence_after();
-      if (tstamp && lane == 0) tstamp[2] = gtimer();
-      const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
-      const uint32_t kv_addr = __shfl_sync(0xffffffffu, ptx::smem_u32(kv_s), 0);
-      const uint32_t q_addr = __shfl_sync(0xffffffffu, ptx::smem_u32(q_s), 0);
-      int s_kv = 0;
-      uint32_t ph_kv = 0;
-      auto advance = [&]() {
-        if (++s_kv == C::NST) { s_kv = 0; ph_kv ^= 1u; }
-      };
-      for (int64_t j = 0; j <= count; ++j) {
-        if (j < count) {
-          if (P.mode != 3) ptx::mbar_wait(kv_full + s_kv, ph_kv);
-          if (trace && lane == 0 && j < 64) trace[j * 8 + 0] = clock64();
-          ptx::tc_fence_after();
-          const uint32_t d_tmem = tm + (uint32_t)((j % C::NS) * BKV);
-          const uint32_t kb = kv_addr + (uint32_t)(s_kv * C::STAGE);
-          if (ptx::elect_one()) {
-#pragma unroll
-            for (int k = 0; k < D / 16; ++k) {
-              const uint32_t off = (uint32_t)((k % 4) * 32);   // 16 bf16 = 32 B inside the 128 B row
-              const uint64_t b = ptx::sw128_desc(kb + (k / 4) * C::KV_PANEL + off, 16, 1024);
-              if (QTM) {
-                ptx::mma_ts(d_tmem, tm + C::Q_COL + k * 8, b, C::IDESC_S, k > 0);
-              } else {
-                const uint64_t a = ptx::sw128_desc(q_addr + (k / 4) * C::Q_PANEL + off, 16, 1024);
-                ptx::mma_ss(d_tmem, a, b, C::IDESC_S, k > 0);
-              }
-            }
-            ptx::tc_commit(kv_empty + s_kv);
-            ptx::tc_commit(s_full + (j % C::NS));
-          }
-          __syncwarp();
-          advance();
-        }
-        if (j >= 1) {
-          const int64_t jj = j - 1;
-          if (P.mode < 3) ptx::mbar_wait(p_full + (jj % C::NS), (uint32_t)((jj / C::NS) & 1));
-          if (trace && lane == 0 && jj < 64) trace[jj * 8 + 1] = clock64();
-          if (P.mode != 3) ptx::mbar_wait(kv_full + s_kv, ph_kv);
-          if (trace && lane == 0 && jj < 64) trace[jj * 8 + 2] = clock64();
-          ptx::tc_fence_after();
-          const uint32_t a_tmem = tm + (uint32_t)((jj % C::NS) * BKV);
-          const uint32_t vb = kv_addr + (uint32_t)(s_kv * C::STAGE);
-          if (ptx::elect_one()) {
-#pragma unroll
-            for (int k = 0; k < BKV / 16; ++k) {
-              const uint64_t b = VT ? ptx::sw128_desc(vb + (k / 4) * C::VT_PANEL + (k % 4) * 32, 16, 1024)
-                                    : ptx::sw128_desc(vb + k * 2048, C::KV_PANEL, 1024);
-              ptx::mma_ts(tm + C::O_COL, a_tmem + k * 8, b, C::IDESC_O, (jj > 0 || k > 0) ? 1u : 0u);
-            }
-            ptx::tc_commit(kv_empty + s_kv);
-            ptx::tc_commit(pv_done);
-          }
-          __syncwarp();
-          advance();
-        }
-      }
-      if (P.mode >= 3 && P.mode <= 4) ptx::mbar_wait(pv_done, (uint32_t)((count - 1) & 1));
-      if (tstamp && lane == 0) tstamp[3] = gtimer();
-    }
-  } else if (warp >= 4) {
-    // ===================== softmax + epilogue =====================
-    // Two warps per TMEM lane quadrant: `half` 0 owns columns [0, B/2) of its
-    // 32 rows, half 1 columns [B/2, B); the row maximum is exchanged through
-    // shared memory once per step, the row sum only at the end.
-    constexpr int HC = BKV / 2;     // score columns per thread
-    constexpr int HD = D / 2;       // output columns per thread
-    const int sw = warp - 4;
-    const int quad = sw & 3, half = sw >> 2;
-    const int row = quad * 32 + lane;
-    const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
-    const int sub = row / (int)g.B;          // which member query block of the tile
-    float m_run = -INFINITY, l_part = 0.f;
-    const float sl2 = P.scale_log2;
-    if (QTM && count > 0) {
-      // Q row -> TMEM lanes (A operand of S = Q K^T): this thread packs half
-      // of its row's d columns, bf16 pairs per 32-bit column
-      constexpr int QW = D / 4;                 // 32-bit words per thread
-      uint32_t qw[QW];
-      const int64_t grow = q_row0 + row;
-      const uint4* src = reinterpret_cast<const uint4*>(P.q + (h * g.T + grow) * D + half * (D / 2));
-      const uint64_t once = ptx::policy_evict_first();   // each Q row is read by one tile only
-#pragma unroll
-      for (int i = 0; i < QW / 4; ++i) {
-        const uint4 x = grow < g.T ? ptx::ld_stream(src + i, once) : make_uint4(0, 0, 0, 0);
-        qw[4 * i] = x.x; qw[4 * i + 1] = x.y; qw[4 * i + 2] = x.z; qw[4 * i + 3] = x.w;
-      }
-      if constexpr (QW == 32) {
-        ptx::tmem_st32(lane_base + C::Q_COL + half * QW, qw);
-      } else {
-        ptx::tmem_st16(lane_base + C::Q_COL + half * QW, qw);
-      }
-      ptx::tmem_st_wait();
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(q_full);
-    }
-    const int64_t sm_count = (P.mode >= 2 && P.mode <= 4) ? 0 : count;
-    for (int64_t j = 0; j < sm_count; ++j) {
-      int64_t m;
-      bool member;
-      if (list) {
-        const int32_t e = list[j];
-        m = e & 0xFFFFFF;
-        member = BKV == 128 || ((e >> (24 + sub)) & 1);   // plain kv-list entries at B = 128
-      } else {
-        m = m_first + j;
-        member = true;
-      }
-      const int len = (int)kv_len(g, m);
-      ptx::mbar_wait(s_full + (j % C::NS), (uint32_t)((j / C::NS) & 1));
-      if (trace && sw == 0 && lane == 0 && j < 64) trace[j * 8 + 3] = clock64();
-      ptx::tc_fence_after();
-      if (P.mode == 1) {  // diagnostic: no softmax math
-        ptx::mbar_arrive(p_full + (j % C::NS));
-        continue;
-      }
-      const uint32_t s_addr = lane_base + (uint32_t)((j % C::NS) * BKV);
-      uint32_t sr[HC / 32][32];
-#pragma unroll
-      for (int c = 0; c < HC / 32; ++c) ptx::tmem_ld32(s_addr + half * HC + c * 32, sr[c]);
-      ptx::tmem_ld_wait();
-      if (!member || len < BKV) {
-#pragma unroll
-        for (int c = 0; c < HC / 32; ++c)
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (!member || half * HC + c * 32 + i >= len) sr[c][i] = __float_as_uint(-INFINITY);
-      }
-      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-      for (int c = 0; c < HC / 32; ++c)
-#pragma unroll
-        for (int i = 0; i < 32; ++i) mx4[i & 3] = fmaxf(mx4[i & 3], __uint_as_float(sr[c][i]));
-      float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
-      red_max[(j & 1) * 256 + half * 128 + row] = mx;
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      if (trace && sw == 0 && lane == 0 && j < 64) trace[j * 8 + 4] = clock64();
-      mx = fmaxf(mx, red_max[(j & 1) * 256 + (half ^ 1) * 128 + row]);
-      const float m_blk = mx * sl2;              // -inf if the row retains nothing here
-      const float m_old = m_run;
-      float alpha = 1.f;
-      bool rescale_o = false;
-      if (m_blk > m_run + kRescaleThreshold || (m_run == -INFINITY && m_blk > -INFINITY)) {
-        alpha = (m_old == -INFINITY) ? 0.f : ptx::ex2(m_old - m_blk);
-        rescale_o = (m_old != -INFINITY) && j > 0;
-        m_run = m_blk;
-      }
-      const float base_m = (m_run == -INFINITY) ? 0.f : m_run;
-      // packed pairs: one FFMA2 (scale, subtract), two ex2, one FADD2 (row
-      // sum), one bf16x2 pack per two scores
-      const float2 sc2 = make_float2(sl2, sl2), nb2 = make_float2(-base_m, -base_m);
-      float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll
-      for (int c = 0; c < HC / 32; ++c) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          // EMU of every 8 element pairs go to the FMA pipe, the rest to MUFU
-          const bool emu = (i & 7) < EMU;
-          const float2 x = ptx::ffma2(make_float2(__uint_as_float(sr[c][2 * i]), __uint_as_float(sr[c][2 * i + 1])),
-                                      sc2, nb2);
-          const float2 p = emu ? ptx::ex2_poly2(x) : make_float2(ptx::ex2(x.x), ptx::ex2(x.y));
-          sum2[i & 1] = ptx::fadd2(sum2[i & 1], p);
-          pk[i] = ptx::pack_bf16(p.x, p.y);
-        }
-        ptx::tmem_st16(s_addr + half * (HC / 2) + c * 16, pk);
-      }
-      const float2 st2 = ptx::fadd2(sum2[0], sum2[1]);
-      l_part = l_part * alpha + (st2.x + st2.y);
-      // tcgen05.ld/st are warp-collective (.sync.aligned): the correction runs
-      // for the whole warp whenever any of its rows needs it
-      if (__any_sync(0xffffffffu, rescale_o)) {
-        // O must hold exactly PV_0..PV_{j-1} before it is rescaled
-        ptx::mbar_wait(pv_done, (uint32_t)((j - 1) & 1));
-        ptx::tc_fence_after();
-        const float a = rescale_o ? alpha : 1.f;
-#pragma unroll
-        for (int c = 0; c < HD / 32; ++c) {
-          uint32_t o[32];
-          const uint32_t oa = lane_base + C::O_COL + half * HD + c * 32;
-          ptx::tmem_ld32(oa, o);
-          ptx::tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * a);
-          ptx::tmem_st32(oa, o);
-        }
-      }
-      ptx::tmem_st_wait();
-      ptx::tc_fence_before();
-      if (trace && sw == 0 && lane == 0 && j < 64) trace[j * 8 + 5] = clock64();
-      ptx::mbar_arrive(p_full + (j % C::NS));
-    }
-
-    // ---- epilogue: O / l, rectification (rectify.py:66-89), bf16 store, LSE ----
-    if (tstamp && sw == 0 && lane == 0) tstamp[4] = gtimer();
-    red_max[512 + half * 128 + row] = l_part;
-    asm volatile("bar.sync 1, 256;" ::: "memory");
-    const float l_run = l_part + red_max[512 + (half ^ 1) * 128 + row];
-    if (sm_count > 0) {
-      ptx::mbar_wait(pv_done, (uint32_t)((count - 1) & 1));
-      ptx::tc_fence_after();
-    }
-    const bool valid = row < rows_valid;
-    const int64_t grow = q_row0 + row;
-    if (text) {
-      // split-K text chunk: unnormalised O (fp32), row max (log2 domain) and
-      // row sum of this chunk; text_combine_kernel produces the output row
-      float* po = P.text_part + (part * 128 + row) * D;
-#pragma unroll
-      for (int c = 0; c < HD / 32; ++c) {
-        uint32_t o[32];
-        const int col0 = half * HD + c * 32;
-        ptx::tmem_ld32(lane_base + C::O_COL + col0, o);
-        ptx::tmem_ld_wait();
-        if (valid) {
-#pragma unroll
-          for (int v4 = 0; v4 < 8; ++v4)
-            *reinterpret_cast<uint4*>(po + col0 + v4 * 4) =
-                make_uint4(o[v4 * 4], o[v4 * 4 + 1], o[v4 * 4 + 2], o[v4 * 4 + 3]);
-        }
-      }
-      if (valid && half == 0) P.text_ml[part * 128 + row] = make_float2(m_run, l_run);
-    } else {
-    float rfac = 1.f;
-    const double* comp = nullptr;
-    if (P.rectify && valid) {
-      const int64_t n_blk = grow / g.B;
-      rfac = P.ws.r_eff[h * g.N + n_blk];
-      comp = P.ws.comp + (h * g.N + n_blk) * D;
-    }
-    const float inv_l = (count > 0 && l_run > 0.f) ? 1.f / l_run : 0.f;
-    __nv_bfloat16* orow = P.out + (h * g.T + grow) * D;
-    const uint64_t once = ptx::policy_evict_first();
-#pragma unroll
-    for (int c = 0; c < HD / 32; ++c) {
-      uint32_t o[32];
-      const int col0 = half * HD + c * 32;
-      ptx::tmem_ld32(lane_base + C::O_COL + col0, o);
-      ptx::tmem_ld_wait();
-      if (valid) {
-#pragma unroll
-        for (int v8 = 0; v8 < 4; ++v8) {
-          uint32_t w[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int col = col0 + v8 * 8 + 2 * i;
-            float y0 = inv_l == 0.f ? 0.f : __uint_as_float(o[v8 * 8 + 2 * i]) * inv_l * rfac;
-            float y1 = inv_l == 0.f ? 0.f : __uint_as_float(o[v8 * 8 + 2 * i + 1]) * inv_l * rfac;
-            if (comp) {
-              y0 += (float)comp[col];
-              y1 += (float)comp[col + 1];
-            }
-            w[i] = ptx::pack_bf16(y0, y1);
-          }
-          ptx::st_stream(orow + col0 + v8 * 8, make_uint4(w[0], w[1], w[2], w[3]), once);
-        }
-      }
-    }
-    if (tstamp && sw == 0 && lane == 0) tstamp[5] = gtimer();
-    if (valid && half == 0 && P.lse && !tstamp)
-      P.lse[h * g.T + grow] = l_run > 0.f ? (log2f(l_run) + m_run) * 0.69314718055994531f : -INFINITY;
-    }
-  }
-
-  __syncwarp();
-  ptx::tc_fence_before();
-  __syncthreads();
-  if (tstamp && threadIdx.x == 0) tstamp[6] = gtimer();
-  if (warp == 2) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc<C::TMEM_COLS>(tmem);
-  }
-}
 
 // ============================================================================
 // Persistent variant (production path): one CTA per SM walks the tiles
@@ -573,7 +126,7 @@ __device__ __forceinline__ void producer_loop(const CUtensorMap& tm_q, const CUt
                                    int64_t n_tiles, uint8_t* kv_s, uint64_t* q_full, uint64_t* kv_full,
                                    uint64_t* kv_empty, uint64_t* s_full, uint64_t* p_full, uint64_t* pv_done,
                                    uint32_t tmem, int lane) {
-  using C = Cfg<D, BKV, true, false>;
+  using C = Cfg<D, BKV>;
   const Geometry& g = P.g;
   (void)g; (void)q_full; (void)s_full; (void)p_full; (void)pv_done; (void)tmem; (void)tm_v;
   // ===================== TMA producer: every tile's [Q] K_0 K_1 V_0 K_2 V_1 ... =====================
@@ -622,7 +175,7 @@ __device__ __forceinline__ void mma_loop(const CUtensorMap& tm_k, const CUtensor
                                    int64_t n_tiles, uint8_t* kv_s, uint64_t* q_full, uint64_t* kv_full,
                                    uint64_t* kv_empty, uint64_t* s_full, uint64_t* p_full, uint64_t* pv_done,
                                    uint32_t tmem, int lane) {
-  using C = Cfg<D, BKV, true, false>;
+  using C = Cfg<D, BKV>;
   const Geometry& g = P.g;
   (void)g; (void)q_full; (void)s_full; (void)p_full; (void)pv_done; (void)tmem; (void)tm_v;
   // ===================== MMA issuer (whole warp; one elected lane issues) =====================
@@ -667,8 +220,7 @@ __device__ __forceinline__ void mma_loop(const CUtensorMap& tm_k, const CUtensor
       }
       if (j >= 1) {
         const int64_t gj = gs + j - 1;
-        if (P.mma_spin) ptx::mbar_spin(p_full + (gj % C::NS), (uint32_t)((gj / C::NS) & 1));
-        else ptx::mbar_wait(p_full + (gj % C::NS), (uint32_t)((gj / C::NS) & 1));
+        ptx::mbar_wait(p_full + (gj % C::NS), (uint32_t)((gj / C::NS) & 1));
         ptx::mbar_wait(kv_full + s_kv, ph_kv);
         ptx::tc_fence_after();
         const uint32_t a_tmem = tm + (uint32_t)((gj % C::NS) * BKV);
@@ -694,11 +246,11 @@ __device__ __forceinline__ void mma_loop(const CUtensorMap& tm_k, const CUtensor
   }
 }
 
-template <int D, int BKV, int WPQ, int EMU>
+template <int D, int BKV, int WPQ>
 __global__ void __launch_bounds__(128 + 128 * WPQ, 1)
 attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                           const __grid_constant__ CUtensorMap tm_v, const TcParams P, int64_t n_tiles) {
-  using C = Cfg<D, BKV, true, false>;
+  using C = Cfg<D, BKV>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* kv_s = base;
@@ -715,10 +267,6 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
 
   const Geometry& g = P.g;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  // RSA_TC_STAMPS=4: per-CTA globaltimer at start / end into `lse` (load-balance profiling)
-  unsigned long long* cta_stamp =
-      (P.stamps == 4 && P.lse) ? reinterpret_cast<unsigned long long*>(P.lse) + 2 * blockIdx.x : nullptr;
-  if (cta_stamp && threadIdx.x == 0) cta_stamp[0] = gtimer();
 
   if (threadIdx.x == 0) {
     ptx::mbar_init(q_full, 128 * WPQ);
@@ -807,10 +355,6 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
       t = decode_tile(P, bid);
       store_q(t);
     }
-    // RSA_TC_STAMPS=3: per-tile clock64 stamps of CTA trace_cta (profiling):
-    // [tile][0] first S ready, [1] last P done, [2] next Q stored, [3] epilogue done
-    long long* tt = (P.stamps == 3 && P.lse && blockIdx.x == (unsigned)P.trace_cta && sw == 0 && lane == 0)
-                        ? reinterpret_cast<long long*>(P.lse) : nullptr;
     int tix = 0;
     for (; bid < n_tiles; bid += gridDim.x, ++tix) {
       const int64_t count = t.count;
@@ -828,9 +372,7 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
           member = true;
         }
         const int len = (int)kv_len(g, m);
-        if (P.sm_spin) ptx::mbar_spin(s_full + (gj % C::NS), (uint32_t)((gj / C::NS) & 1));
-        else ptx::mbar_wait(s_full + (gj % C::NS), (uint32_t)((gj / C::NS) & 1));
-        if (tt && j == 0 && tix < 256) tt[tix * 4 + 0] = clock64();
+        ptx::mbar_wait(s_full + (gj % C::NS), (uint32_t)((gj / C::NS) & 1));
         ptx::tc_fence_after();
         const uint32_t s_addr = lane_base + (uint32_t)((gj % C::NS) * BKV);
         uint32_t sr[HC / 32][32];
@@ -873,8 +415,7 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
           for (int i = 0; i < 16; ++i) {
             const float2 x = ptx::ffma2(make_float2(__uint_as_float(sr[c][2 * i]), __uint_as_float(sr[c][2 * i + 1])),
                                         sc2, nb2);
-            // EMU of every 8 pairs on the FMA pipe (polynomial), the rest on MUFU
-            const float2 p = (i & 7) < EMU ? ptx::ex2_poly2(x) : make_float2(ptx::ex2(x.x), ptx::ex2(x.y));
+            const float2 p = make_float2(ptx::ex2(x.x), ptx::ex2(x.y));
             sum2[i & 1] = ptx::fadd2(sum2[i & 1], p);
             pk[i] = ptx::pack_bf16(p.x, p.y);
           }
@@ -904,14 +445,12 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
       }
       // every S of this tile has been read: Q's TMEM columns are free, so the
       // next tile's Q goes in now and its S_0, S_1 overlap this epilogue
-      if (tt && tix < 256) tt[tix * 4 + 1] = clock64();
       const TileDesc cur = t;
       const int64_t nb = bid + gridDim.x;
       if (nb < n_tiles) {
         t = decode_tile(P, nb);
         store_q(t);
       }
-      if (tt && tix < 256) tt[tix * 4 + 2] = clock64();
 
       // ---- epilogue: O / l, rectification (rectify.py:66-89), bf16 store, LSE ----
       red_max[2 * WPQ * 128 + half * 128 + row] = l_part;
@@ -977,12 +516,11 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
             }
           }
         }
-        if (valid && half == 0 && P.lse && !P.stamps)
+        if (valid && half == 0 && P.lse)
           P.lse[cur.h * g.T + orig] = l_run > 0.f ? (log2f(l_run) + m_run) * 0.69314718055994531f : -INFINITY;
       }
       // O is read: the next tile's PV_0 (after its P_0 below) may overwrite it
       ptx::tc_fence_before();
-      if (tt && tix < 256) tt[tix * 4 + 3] = clock64();
       gs += count;
     }
   }
@@ -990,7 +528,6 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
   __syncwarp();
   ptx::tc_fence_before();
   __syncthreads();
-  if (cta_stamp && threadIdx.x == 0) cta_stamp[1] = gtimer();
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<C::TMEM_COLS>(tmem);
@@ -1040,52 +577,11 @@ __global__ void __launch_bounds__(256) text_combine_kernel(const float* __restri
   if (lse && half == 0) lse[h * g.T + g.Tv + trow] = l > 0.f ? (log2f(l) + mx) * 0.69314718055994531f : -INFINITY;
 }
 
-// V [H][T][d] -> V^T [H][d][T] through a padded 64x64 shared-memory tile
-__global__ void __launch_bounds__(256) transpose_v_kernel(const __nv_bfloat16* __restrict__ v,
-                                                          __nv_bfloat16* __restrict__ vt, int64_t T,
-                                                          int64_t pitch, int64_t d) {
-  __shared__ __nv_bfloat16 tile[64][72];
-  const int64_t h = blockIdx.z, t0 = (int64_t)blockIdx.x * 64, c0 = (int64_t)blockIdx.y * 64;
-  const __nv_bfloat16* src = v + h * T * d;
-  for (int i = threadIdx.x; i < 64 * 8; i += 256) {
-    const int r = i / 8, cc = (i % 8) * 8;
-    uint4 x = make_uint4(0, 0, 0, 0);
-    if (t0 + r < T) x = __ldg(reinterpret_cast<const uint4*>(src + (t0 + r) * d + c0 + cc));
-    *reinterpret_cast<uint4*>(&tile[r][cc]) = x;
-  }
-  __syncthreads();
-  __nv_bfloat16* dst = vt + h * d * pitch;
-  for (int i = threadIdx.x; i < 64 * 8; i += 256) {
-    const int c = i / 8, rr = (i % 8) * 8;
-    if (t0 + rr + 8 <= T) {
-      __align__(16) __nv_bfloat16 w[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) w[k] = tile[rr + k][c];
-      *reinterpret_cast<uint4*>(dst + (c0 + c) * pitch + t0 + rr) = *reinterpret_cast<const uint4*>(w);
-    } else {
-      for (int k = 0; k < 8 && t0 + rr + k < T; ++k) dst[(c0 + c) * pitch + t0 + rr + k] = tile[rr + k][c];
-    }
-  }
-}
-
-int64_t vt_pitch(const Geometry& g) { return (g.T + 7) / 8 * 8; }
-
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
-  return fn;
-}
 
 // 3-D bf16 tensor [dim2][dim1][dim0] (dim0 contiguous), box (64, box1, 1), 128B swizzle
 bool make_tmap_3d(CUtensorMap* tm, const void* ptr, int64_t dim0, int64_t dim1, int64_t dim2, int box1,
                   int64_t pitch0 = 0) {
-  auto fn = encode_fn();
+  auto fn = tmap_encode_fn();
   if (!fn) return false;
   if (pitch0 == 0) pitch0 = dim0;
   cuuint64_t dims[3] = {(cuuint64_t)dim0, (cuuint64_t)dim1, (cuuint64_t)dim2};
@@ -1099,7 +595,7 @@ bool make_tmap_3d(CUtensorMap* tm, const void* ptr, int64_t dim0, int64_t dim1, 
 }
 
 // ============================================================================
-// Ping-pong kernel (default for d = B = 128; RSA_TC_PP=0 disables): two query tiles per CTA in
+// Ping-pong kernel (d = B = 128): two query tiles per CTA in
 // independent "slots", FA4-style.  Each slot has its own Q (shared memory, SS
 // MMA for S), K/V ring, S/P and O TMEM columns (2 x (128 + 128) = 512), TMA
 // producer warp, MMA warp and softmax warpgroup with one thread per row (no
@@ -1133,7 +629,6 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
   // per slot: q_full, q_empty, kv_full[2], kv_empty[2], s_full[2], pv_done, p_full[2], o_full  (12 barriers)
   auto slot_bar = [&](int s, int i) { return bars + s * 12 + i; };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
-  int* issue_lock = reinterpret_cast<int*>(bars + 25);   // (pp_lock) one slot's MMA group at a time
   float* comp_s = reinterpret_cast<float*>(bars + 64);   // [slot][tile parity][D] compensation rows
 
   const Geometry& g = P.g;
@@ -1153,7 +648,6 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
       ptx::mbar_init(slot_bar(s, 10), 128);  // p_full[1]
       ptx::mbar_init(slot_bar(s, 11), 1);    // o_full: the tile's last PV is complete
     }
-    *issue_lock = 0;
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc<512>(tmem_slot);
@@ -1214,14 +708,6 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
     int st = 0;          // ring stage of the current kv block's K (V is the next stage)
     uint32_t ph = 0, qph = 0;
     int64_t gi = 0;      // sub-steps before the current tile
-    auto stage_of = [&](int64_t blk_in_tile, int kv, int& st_out, uint32_t& ph_out) {
-      // K_j and V_j occupy consecutive ring slots: index 2j (+1)
-      const int64_t idx = 2 * blk_in_tile + kv;
-      (void)idx;
-      st_out = st;
-      ph_out = ph;
-    };
-    (void)stage_of;
     for (int64_t bid = 2 * (int64_t)blockIdx.x + s; bid < n_tiles; bid += stride) {
       const int64_t count = decode_tile(P, bid).count;
       const int64_t nsub = 2 * count;
@@ -1245,9 +731,6 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
         const uint32_t kb = ring + (uint32_t)(sj * C::STAGE) + (uint32_t)(half * 64 * 128);
         const uint32_t d_tmem = tm + (uint32_t)(half * 64);
         if (ptx::elect_one()) {
-          if (P.pp_lock)
-            while (atomicCAS(issue_lock, 0, 1) != 0) {
-            }
 #pragma unroll
           for (int k = 0; k < D / 16; ++k) {
             const uint32_t off = (uint32_t)((k / 4) * C::Q_PANEL + (k % 4) * 32);
@@ -1258,7 +741,6 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
           if (half == 1) ptx::tc_commit(slot_bar(s, 4 + sj));   // K_j fully read
           ptx::tc_commit(slot_bar(s, 6 + half));                  // s_full[half]
           if (i == nsub - 1) ptx::tc_commit(slot_bar(s, 1));      // Q may be replaced after this
-          if (P.pp_lock) atomicExch(issue_lock, 0);
         }
         __syncwarp();
       };
@@ -1284,9 +766,6 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
         ptx::tc_fence_after();
         const uint32_t vb = ring + (uint32_t)(sv * C::STAGE) + (uint32_t)(half * 64 * 128);
         if (ptx::elect_one()) {
-          if (P.pp_lock)
-            while (atomicCAS(issue_lock, 0, 1) != 0) {
-            }
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const uint64_t b = ptx::sw128_desc(vb + k * 2048, C::KV_PANEL, 1024);
@@ -1294,7 +773,6 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
           }
           if (half == 1) ptx::tc_commit(slot_bar(s, 4 + sv));   // V_j fully read
           ptx::tc_commit(slot_bar(s, 8));                         // pv_done
-          if (P.pp_lock) atomicExch(issue_lock, 0);
         }
         __syncwarp();
         if (i + 2 < nsub) issue_s(i + 2);
@@ -1505,8 +983,6 @@ cudaError_t launch_pp(const Geometry& g, const void* q, const void* k, const voi
   P.text_part = ws.text_part;
   P.text_ml = reinterpret_cast<float2*>(ws.text_ml);
   P.scale_log2 = (float)(1.4426950408889634 / sqrt((double)g.d));
-  static const int lock_env = [] { const char* e = getenv("RSA_TC_PP_LOCK"); return e ? atoi(e) : 0; }();
-  P.pp_lock = lock_env;
   cudaError_t e = cudaFuncSetAttribute(attn_tc_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
@@ -1522,23 +998,19 @@ cudaError_t launch_pp(const Geometry& g, const void* q, const void* k, const voi
   return cudaGetLastError();
 }
 
-template <int D, int BKV, int WPQ, int EMU = 0>
+template <int D, int BKV, int WPQ>
 cudaError_t launch_persistent(const Geometry& g, const void* q, const void* k, const void* v, void* out,
                               float* lse, const Workspace& ws, bool rectify, bool text, cudaStream_t st,
                               const int32_t* perm) {
-  using C = Cfg<D, BKV, true, false>;
+  using C = Cfg<D, BKV>;
   CUtensorMap tq, tk, tv;
   if (!make_tmap_3d(&tq, q, g.d, g.T, g.H, 128) || !make_tmap_3d(&tk, k, g.d, g.T, g.H, BKV) ||
       !make_tmap_3d(&tv, v, g.d, g.T, g.H, BKV))
     return cudaErrorInvalidValue;
   TcParams P{};
   // Q through the ring when a Q tile is exactly one stage (BKV = 128) and rows
-  // are not gathered through a permutation; RSA_TC_QRING=0 loads Q rows directly
-  static const int qring_env = [] { const char* e = getenv("RSA_TC_QRING"); return e ? atoi(e) : 1; }();
-  P.qring = (qring_env != 0 && C::STAGE == C::Q_BYTES && perm == nullptr) ? 1 : 0;
-  static const int spin_env = [] { const char* e = getenv("RSA_TC_SPIN"); return e ? atoi(e) : 0; }();
-  P.mma_spin = spin_env & 1;
-  P.sm_spin = (spin_env >> 1) & 1;
+  // are not gathered through a permutation
+  P.qring = (C::STAGE == C::Q_BYTES && perm == nullptr) ? 1 : 0;
   P.g = g;
   P.ws = ws;
   P.out = static_cast<__nv_bfloat16*>(out);
@@ -1554,11 +1026,7 @@ cudaError_t launch_persistent(const Geometry& g, const void* q, const void* k, c
   P.text_part = ws.text_part;
   P.text_ml = reinterpret_cast<float2*>(ws.text_ml);
   P.scale_log2 = (float)(1.4426950408889634 / sqrt((double)g.d));
-  const char* sp = getenv("RSA_TC_STAMPS");
-  P.stamps = sp ? atoi(sp) : 0;
-  const char* tc_cta = getenv("RSA_TC_TRACE_CTA");
-  P.trace_cta = tc_cta ? atoi(tc_cta) : 0;
-  auto kern = attn_tc_persistent_kernel<D, BKV, WPQ, EMU>;
+  auto kern = attn_tc_persistent_kernel<D, BKV, WPQ>;
   const int smem = C::SMEM - 768 * 4 + 3 * WPQ * 128 * 4;   // row-max / row-sum exchange area
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
@@ -1574,114 +1042,30 @@ cudaError_t launch_persistent(const Geometry& g, const void* q, const void* k, c
   return cudaGetLastError();
 }
 
-template <int D, int BKV, bool QTM, bool VT, int EMU>
-cudaError_t launch_cfg(const Geometry& g, const void* q, const void* k, const void* v, void* out, float* lse,
-                       const Workspace& ws, bool rectify, bool text, cudaStream_t st) {
-  using C = Cfg<D, BKV, QTM, VT>;
-  CUtensorMap tq, tk, tv;
-  // V^T (K-major B operand of the PV MMA: mixing K- and MN-major B operands
-  // in one MMA stream costs ~35% tensor throughput on sm_100a, measured)
-  if (VT) {
-    dim3 tg((unsigned)((g.T + 63) / 64), (unsigned)(g.d / 64), (unsigned)g.H);
-    transpose_v_kernel<<<tg, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(v), ws.v_t, g.T, vt_pitch(g), g.d);
-  }
-  if (!make_tmap_3d(&tq, q, g.d, g.T, g.H, 128) || !make_tmap_3d(&tk, k, g.d, g.T, g.H, BKV) ||
-      !(VT ? make_tmap_3d(&tv, ws.v_t, g.T, g.d, g.H, D, vt_pitch(g)) : make_tmap_3d(&tv, v, g.d, g.T, g.H, BKV)))
-    return cudaErrorInvalidValue;
-  TcParams P;
-  P.g = g;
-  P.ws = ws;
-  P.out = static_cast<__nv_bfloat16*>(out);
-  P.q = static_cast<const __nv_bfloat16*>(q);
-  const char* md = getenv("RSA_TC_MODE");
-  P.mode = md ? atoi(md) : 0;
-  const char* sp = getenv("RSA_TC_STAMPS");
-  P.stamps = sp ? atoi(sp) : 0;
-  const char* tc_cta = getenv("RSA_TC_TRACE_CTA");
-  P.trace_cta = tc_cta ? atoi(tc_cta) : 5000;
-  P.lse = lse;
-  P.rectify = rectify ? 1 : 0;
-  P.text_tiles_per_head = text ? (g.Tt + 127) / 128 : 0;
-  P.text_chunks = text_chunks(g);
-  P.chunk_blocks = (g.M + P.text_chunks - 1) / P.text_chunks;
-  P.video_tiles_per_head = (g.N * g.B + 127) / 128;
-  P.tiles_per_head = P.text_tiles_per_head * P.text_chunks + P.video_tiles_per_head;
-  P.text_part = ws.text_part;
-  P.text_ml = reinterpret_cast<float2*>(ws.text_ml);
-  P.scale_log2 = (float)(1.4426950408889634 / sqrt((double)g.d));
-  auto kern = attn_tc_kernel<D, BKV, QTM, VT, EMU>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-  if (e != cudaSuccess) return e;
-  kern<<<(unsigned)(g.H * P.tiles_per_head), kThreads, C::SMEM, st>>>(tq, tk, tv, P);
-  e = cudaGetLastError();
-  if (e != cudaSuccess || P.text_tiles_per_head == 0) return e;
-  text_combine_kernel<D><<<(unsigned)(g.H * P.text_tiles_per_head), 256, 0, st>>>(
-      P.text_part, P.text_ml, P.out, lse, g, P.text_tiles_per_head, P.text_chunks);
-  return cudaGetLastError();
-}
 
 }  // namespace
 
 bool tc_supported(const Geometry& g) {
   return g.dtype == RSA_BF16 && (g.d == 64 || g.d == 128) && (g.B == 64 || g.B == 128) &&
-         g.T * g.d < (int64_t(1) << 31) && g.H < 65536 && encode_fn() != nullptr;
+         g.T * g.d < (int64_t(1) << 31) && g.H < 65536 && tmap_encode_fn() != nullptr;
 }
 
 cudaError_t launch_attn_tc(const Geometry& g, const void* q, const void* k, const void* v, void* out, float* lse,
                            const Workspace& ws, bool rectify, bool text, cudaStream_t st, int* launches,
-                           const int32_t* perm, const void* q_perm) {
-  static const bool vt_on = [] { const char* e = getenv("RSA_TC_VT"); return e && atoi(e) != 0; }();
-  *launches += (vt_on ? 2 : 1) + (text && g.Tt > 0 ? 1 : 0);   // (V transpose) + attention (+ text combine)
-  // Variant knobs (profiling): RSA_TC_QTMEM=1 keeps Q in TMEM (2 S buffers);
-  // RSA_TC_VT=0 streams V as an MN-major operand instead of V^T.
-  static const int qtm = [] { const char* e = getenv("RSA_TC_QTMEM"); return e ? atoi(e) : 1; }();
-  static const int vt = [] { const char* e = getenv("RSA_TC_VT"); return e ? atoi(e) : 0; }();
-  // RSA_TC_EMU=n: n of every 8 exp2 pairs on the FMA pipe (polynomial) instead of MUFU
-  static const int emu = [] { const char* e = getenv("RSA_TC_EMU"); return e ? atoi(e) : 0; }();
-  const int sel = (qtm ? 2 : 0) + (vt ? 1 : 0);
-  // RSA_TC_PERSIST=0: one CTA per tile (attn_tc_kernel, with the diagnostic modes)
-  static const int persist = [] { const char* e = getenv("RSA_TC_PERSIST"); return e ? atoi(e) : 1; }();
-  // RSA_TC_PEMU=n: n of every 8 ex2 pairs on the FMA pipe in the persistent kernel
-  static const int pemu = [] { const char* e = getenv("RSA_TC_PEMU"); return e ? atoi(e) : 0; }();
-  // the two-tile ping-pong kernel for d = B = 128 (RSA_TC_PP=0: the persistent one-tile kernel)
-  static const int pp = [] { const char* e = getenv("RSA_TC_PP"); return e ? atoi(e) : 1; }();
-  // (the permuted problem runs on it with the permuted Q copy K1 wrote)
-  if (pp && g.d == 128 && g.B == 128 && (!perm || q_perm))
+                           const int32_t* perm, const void* q_perm, int kernel) {
+  *launches += 1 + (text && g.Tt > 0 ? 1 : 0);   // attention (+ text combine)
+  // d = B = 128: the ping-pong kernel (the permuted problem runs on it with the
+  // permuted Q copy K1 wrote); RSA_KERNEL_TCGEN05_PERSISTENT asks for the
+  // one-tile persistent kernel instead (cross-checks)
+  if (g.d == 128 && g.B == 128 && kernel != RSA_KERNEL_TCGEN05_PERSISTENT && (!perm || q_perm))
     return launch_pp(g, perm ? q_perm : q, k, v, out, lse, ws, rectify, text, st, perm);
-  if (persist && qtm && !vt && emu == 0) {
-    if (g.d == 128 && g.B == 128 && pemu == 1)
-      return launch_persistent<128, 128, 2, 1>(g, q, k, v, out, lse, ws, rectify, text, st, perm);
-    if (g.d == 128 && g.B == 128 && pemu == 2)
-      return launch_persistent<128, 128, 2, 2>(g, q, k, v, out, lse, ws, rectify, text, st, perm);
 #define RSA_TC_P(DD, BB) \
   if (g.d == DD && g.B == BB) return launch_persistent<DD, BB, 2>(g, q, k, v, out, lse, ws, rectify, text, st, perm);
-    RSA_TC_P(128, 128)
-    RSA_TC_P(128, 64)
-    RSA_TC_P(64, 128)
-    RSA_TC_P(64, 64)
+  RSA_TC_P(128, 128)
+  RSA_TC_P(128, 64)
+  RSA_TC_P(64, 128)
+  RSA_TC_P(64, 64)
 #undef RSA_TC_P
-  }
-  if (perm) return cudaErrorNotSupported;   // the permuted problem runs on the persistent kernel only
-  if (qtm && !vt && g.d == 128 && g.B == 128 && emu == 1)
-    return launch_cfg<128, 128, true, false, 1>(g, q, k, v, out, lse, ws, rectify, text, st);
-  if (qtm && !vt && g.d == 128 && g.B == 128 && emu == 2)
-    return launch_cfg<128, 128, true, false, 2>(g, q, k, v, out, lse, ws, rectify, text, st);
-  if (qtm && !vt && g.d == 128 && g.B == 128 && emu == 3)
-    return launch_cfg<128, 128, true, false, 3>(g, q, k, v, out, lse, ws, rectify, text, st);
-#define RSA_TC_CASE(DD, BB)                                                                          \
-  if (g.d == DD && g.B == BB) {                                                                      \
-    switch (sel) {                                                                                   \
-      case 0: return launch_cfg<DD, BB, false, false, 0>(g, q, k, v, out, lse, ws, rectify, text, st); \
-      case 2: return launch_cfg<DD, BB, true, false, 0>(g, q, k, v, out, lse, ws, rectify, text, st);  \
-      case 3: return launch_cfg<DD, BB, true, true, 0>(g, q, k, v, out, lse, ws, rectify, text, st);   \
-      default: return launch_cfg<DD, BB, false, true, 0>(g, q, k, v, out, lse, ws, rectify, text, st); \
-    }                                                                                                \
-  }
-  RSA_TC_CASE(128, 128)
-  RSA_TC_CASE(128, 64)
-  RSA_TC_CASE(64, 128)
-  RSA_TC_CASE(64, 64)
-#undef RSA_TC_CASE
   return cudaErrorInvalidValue;
 }
 

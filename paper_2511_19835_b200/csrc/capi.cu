@@ -61,6 +61,10 @@ rsa_status make_geometry(const rsa_shape* s, rsa::Geometry* g) {
   g->qt_rows = g->Tt;
   g->qt_row0 = g->Tv;
   g->q_rows = g->T;
+  g->hb = g->H;   // contiguous [H][T][d] (rsa_shape_set_layout may override)
+  g->s_tok = g->d;
+  g->s_head = g->T * g->d;
+  g->s_batch = g->H * g->T * g->d;
   const int64_t dmax = s->dtype == RSA_F64 ? 128 : 256;
   if (g->d > dmax)
     return fail(RSA_ERR_UNSUPPORTED, "head_dim " + std::to_string(g->d) + " > " + std::to_string(dmax));
@@ -106,7 +110,7 @@ void layout_of(const rsa::Geometry& g, rsa_workspace_layout* L) {
   L->kv_list = take(H * N * M * 4);
   L->tile_count = take(H * TT * 4);
   L->tile_list = take(H * TT * M * 4);
-  L->v_t = take(g.dtype == RSA_BF16 ? H * (size_t)((g.T + 7) / 8 * 8) * d * 2 : 0);   // pitch % 8 == 0
+  L->v_t = take(0);   // (unused since round 2; kept for the layout ABI)
   const size_t text_parts = g.dtype == RSA_BF16 ? H * (size_t)((g.Tt + 127) / 128) * rsa::text_chunks(g) * 128 : 0;
   L->text_part = take(text_parts * d * 4);
   L->text_ml = take(text_parts * 8);
@@ -156,14 +160,15 @@ rsa_status run_attention(const rsa_shape* s, const rsa::Geometry& g, const rsa::
   // bf16 runs on the tensor-core kernel; the CUDA-core kernel serves the
   // reference's fp32/fp64 precisions, and bf16 only when asked for by name
   // (a cross-check) -- never as a silent second backend
-  if ((s->kernel == RSA_KERNEL_TCGEN05 || (s->kernel == RSA_KERNEL_AUTO && g.dtype == RSA_BF16)) && !tc)
+  if ((s->kernel == RSA_KERNEL_TCGEN05 || s->kernel == RSA_KERNEL_TCGEN05_PERSISTENT ||
+       (s->kernel == RSA_KERNEL_AUTO && g.dtype == RSA_BF16)) && !tc)
     return fail(RSA_ERR_UNSUPPORTED, "bf16 attention runs on the tcgen05 kernel, which needs block and "
                                      "head_dim in {64, 128} (kernel='simt' selects the CUDA-core kernel "
                                      "explicitly)");
   if (tc) {
     e = rsa::launch_tile_lists(g, ws, st, &g_launches);
     if (e != cudaSuccess) return cuda_fail(e, "tile_lists");
-    e = rsa::launch_attn_tc(g, q, k, v, out, lse, ws, rectify, text, st, &g_launches, perm, q_perm);
+    e = rsa::launch_attn_tc(g, q, k, v, out, lse, ws, rectify, text, st, &g_launches, perm, q_perm, s->kernel);
     if (e != cudaSuccess) return cuda_fail(e, "attn_tc");
   } else {
     if (perm) return fail(RSA_ERR_UNSUPPORTED, "the permuted problem needs the tcgen05 kernel (bf16)");
@@ -428,6 +433,7 @@ rsa_status rsa_text_full_attention(int64_t heads, int64_t n_queries, int64_t n_k
   g.H = heads; g.Tv = s.t_video; g.Tt = s.t_text; g.T = n_keys; g.d = head_dim; g.B = block;
   g.N = g.Tv / block; g.n_text = g.Tt > 0 ? 1 : 0; g.M = g.N + g.n_text;
   g.last_len = g.Tt; g.n_cols = 0; g.dtype = dtype; g.q_last = block;
+  g.hb = heads; g.s_tok = head_dim; g.s_head = n_keys * head_dim; g.s_batch = heads * n_keys * head_dim;
   g.qt_rows = n_queries; g.qt_row0 = 0; g.q_rows = n_queries;
   if (dtype < RSA_BF16 || dtype > RSA_F64) return fail(RSA_ERR_SHAPE, "bad dtype");
   if (head_dim < 1 || head_dim > (dtype == RSA_F64 ? 128 : 256))

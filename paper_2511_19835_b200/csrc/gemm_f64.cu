@@ -9,17 +9,19 @@
 // by summation order -- the same freedom cuBLAS had; the downstream masks are
 // bit-exact by margin (k-th gaps >= 1e-7 relative vs ~1e-16).
 //
-// Tiling: 64 x 64 CTA tile, 4 warps in 2 x 2, each a 32 x 32 warp tile of
-// 4 x 4 DMMA 8x8 fragments; K in steps of 16, staged k-major in shared memory
-// ([k][m], row pitch 72 doubles: the fragment loads of a warp hit every bank
-// pair exactly twice = the 2-wavefront minimum for 256 bytes), double-buffered
-// with the next k-tile prefetched into registers during the current MMAs.
+// Tiling: BM x BN CTA tile of 32 x 32 warp tiles (4 x 4 DMMA 8x8 fragments
+// each); K in steps of 16, staged k-major in shared memory ([k][m], row pitch
+// BM + 8 doubles: the fragment loads of a warp hit every bank pair exactly
+// twice = the 2-wavefront minimum for 256 bytes), double-buffered with the
+// next k-tile prefetched into registers during the current MMAs.  Short-K
+// problems (the scores GEMM, K = d) use 128-row tiles so each CTA's prologue
+// is amortised over twice the MMAs.
 #include "rsa_internal.cuh"
 
 namespace rsa {
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16, PITCH = 72, GT = 128;
+constexpr int BK = 16;
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -33,12 +35,11 @@ struct GemmArgs {
   double* C; int64_t ldc, sC;
 };
 
-// one thread's share of a 64 x 16 tile stored k-contiguous in global memory
-// (A, or B^T): row r = t / 2, eight consecutive k from (t % 2) * 8
+// chunk c (8 consecutive k) of a ROWS x 16 tile stored k-contiguous in global
+// memory (A, or B^T): row c / 2, k offset (c % 2) * 8
 __device__ __forceinline__ void load_kmajor(const double* __restrict__ p, int64_t ld, int64_t rows, int64_t K,
-                                            int64_t r0, int64_t k0, double (&x)[8]) {
-  const int t = threadIdx.x;
-  const int64_t r = r0 + t / 2, k = k0 + (t % 2) * 8;
+                                            int64_t r0, int64_t k0, int c, double (&x)[8]) {
+  const int64_t r = r0 + c / 2, k = k0 + (c % 2) * 8;
   if (r < rows && k + 8 <= K && ((reinterpret_cast<uintptr_t>(p + r * ld + k) & 15) == 0)) {
     const double2* src = reinterpret_cast<const double2*>(p + r * ld + k);
 #pragma unroll
@@ -53,21 +54,21 @@ __device__ __forceinline__ void load_kmajor(const double* __restrict__ p, int64_
   }
 }
 
-__device__ __forceinline__ void store_kmajor(double* s, const double (&x)[8]) {
-  const int t = threadIdx.x;
-  const int m = t / 2, kb = (t % 2) * 8;
+template <int PITCH>
+__device__ __forceinline__ void store_kmajor(double* s, int c, const double (&x)[8]) {
+  const int m = c / 2, kb = (c % 2) * 8;
 #pragma unroll
   for (int i = 0; i < 8; ++i) s[(kb + i) * PITCH + m] = x[i];
 }
 
-// one thread's share of a 16 x 64 tile stored n-contiguous (B of NN): row
-// k = t / 8, eight consecutive n from (t % 8) * 8
+// chunk c (8 consecutive n) of a 16 x COLS tile stored n-contiguous (B of NN):
+// row k = c / (COLS / 8), n offset (c % (COLS / 8)) * 8
+template <int COLS>
 __device__ __forceinline__ void load_nmajor(const double* __restrict__ p, int64_t ld, int64_t cols, int64_t K,
-                                            int64_t c0, int64_t k0, double (&x)[8]) {
-  const int t = threadIdx.x;
-  const int64_t k = k0 + t / 8, c = c0 + (t % 8) * 8;
-  if (k < K && c + 8 <= cols && ((reinterpret_cast<uintptr_t>(p + k * ld + c) & 15) == 0)) {
-    const double2* src = reinterpret_cast<const double2*>(p + k * ld + c);
+                                            int64_t c0, int64_t k0, int c, double (&x)[8]) {
+  const int64_t k = k0 + c / (COLS / 8), n = c0 + (c % (COLS / 8)) * 8;
+  if (k < K && n + 8 <= cols && ((reinterpret_cast<uintptr_t>(p + k * ld + n) & 15) == 0)) {
+    const double2* src = reinterpret_cast<const double2*>(p + k * ld + n);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const double2 v = __ldg(src + i);
@@ -76,28 +77,34 @@ __device__ __forceinline__ void load_nmajor(const double* __restrict__ p, int64_
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) x[i] = (k < K && c + i < cols) ? __ldg(p + k * ld + c + i) : 0.0;
+    for (int i = 0; i < 8; ++i) x[i] = (k < K && n + i < cols) ? __ldg(p + k * ld + n + i) : 0.0;
   }
 }
 
-__device__ __forceinline__ void store_nmajor(double* s, const double (&x)[8]) {
-  const int t = threadIdx.x;
-  double2* dst = reinterpret_cast<double2*>(s + (t / 8) * PITCH + (t % 8) * 8);
+template <int PITCH, int COLS>
+__device__ __forceinline__ void store_nmajor(double* s, int c, const double (&x)[8]) {
+  double2* dst = reinterpret_cast<double2*>(s + (c / (COLS / 8)) * PITCH + (c % (COLS / 8)) * 8);
 #pragma unroll
   for (int i = 0; i < 4; ++i) dst[i] = make_double2(x[2 * i], x[2 * i + 1]);
 }
 
-template <bool NT>
-__global__ void __launch_bounds__(GT) dgemm_kernel(GemmArgs a) {
-  __shared__ __align__(16) double As[2][BK * PITCH];
-  __shared__ __align__(16) double Bs[2][BK * PITCH];
+template <int BM, int BN, bool NT>
+__global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32) dgemm_kernel(GemmArgs a) {
+  constexpr int WN = BN / 32;                   // warps along N
+  constexpr int T = (BM / 32) * WN * 32;
+  constexpr int PA = BM + 8, PB = BN + 8;       // shared-memory pitches (doubles)
+  constexpr int CA = BM * BK / 8, CB = BN * BK / 8;   // 8-double chunks per tile
+  constexpr int RA = (CA + T - 1) / T, RB = (CB + T - 1) / T;
+  extern __shared__ __align__(16) double smem_d[];
+  double* As[2] = {smem_d, smem_d + BK * PA};
+  double* Bs[2] = {smem_d + 2 * BK * PA, smem_d + 2 * BK * PA + BK * PB};
   const int64_t b = blockIdx.z;
   const double* A = a.A + b * a.sA;
   const double* B = a.B + b * a.sB;
   double* C = a.C + b * a.sC;
   const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int t = threadIdx.x, warp = t / 32, lane = t % 32;
+  const int wm = (warp / WN) * 32, wn = (warp % WN) * 32;
   const int g = lane >> 2, tg = lane & 3;
 
   double acc[4][4][2];
@@ -106,16 +113,28 @@ __global__ void __launch_bounds__(GT) dgemm_kernel(GemmArgs a) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  double xa[8], xb[8];
+  double xa[RA][8], xb[RB][8];
   auto fetch = [&](int64_t k0) {
-    load_kmajor(A, a.lda, a.M, a.K, m0, k0, xa);
-    if (NT) load_kmajor(B, a.ldb, a.N, a.K, n0, k0, xb);
-    else load_nmajor(B, a.ldb, a.N, a.K, n0, k0, xb);
+#pragma unroll
+    for (int r = 0; r < RA; ++r)
+      if (t + r * T < CA) load_kmajor(A, a.lda, a.M, a.K, m0, k0, t + r * T, xa[r]);
+#pragma unroll
+    for (int r = 0; r < RB; ++r)
+      if (t + r * T < CB) {
+        if (NT) load_kmajor(B, a.ldb, a.N, a.K, n0, k0, t + r * T, xb[r]);
+        else load_nmajor<BN>(B, a.ldb, a.N, a.K, n0, k0, t + r * T, xb[r]);
+      }
   };
   auto stash = [&](int buf) {
-    store_kmajor(As[buf], xa);
-    if (NT) store_kmajor(Bs[buf], xb);
-    else store_nmajor(Bs[buf], xb);
+#pragma unroll
+    for (int r = 0; r < RA; ++r)
+      if (t + r * T < CA) store_kmajor<PA>(As[buf], t + r * T, xa[r]);
+#pragma unroll
+    for (int r = 0; r < RB; ++r)
+      if (t + r * T < CB) {
+        if (NT) store_kmajor<PB>(Bs[buf], t + r * T, xb[r]);
+        else store_nmajor<PB, BN>(Bs[buf], t + r * T, xb[r]);
+      }
   };
   const int64_t k_tiles = (a.K + BK - 1) / BK;
   fetch(0);
@@ -130,9 +149,9 @@ __global__ void __launch_bounds__(GT) dgemm_kernel(GemmArgs a) {
     for (int kk = 0; kk < BK; kk += 4) {
       double fa[4], fb[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) fa[i] = as[(kk + tg) * PITCH + wm + i * 8 + g];
+      for (int i = 0; i < 4; ++i) fa[i] = as[(kk + tg) * PA + wm + i * 8 + g];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) fb[j] = bs[(kk + tg) * PITCH + wn + j * 8 + g];
+      for (int j = 0; j < 4; ++j) fb[j] = bs[(kk + tg) * PB + wn + j * 8 + g];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -148,9 +167,40 @@ __global__ void __launch_bounds__(GT) dgemm_kernel(GemmArgs a) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int64_t c = n0 + wn + j * 8 + tg * 2;
-      if (c < a.N) C[r * a.ldc + c] = acc[i][j][0];
-      if (c + 1 < a.N) C[r * a.ldc + c + 1] = acc[i][j][1];
+      double* dst = C + r * a.ldc + c;
+      if (c + 1 < a.N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+        *reinterpret_cast<double2*>(dst) = make_double2(acc[i][j][0], acc[i][j][1]);
+      } else {
+        if (c < a.N) dst[0] = acc[i][j][0];
+        if (c + 1 < a.N) dst[1] = acc[i][j][1];
+      }
     }
+  }
+}
+
+template <int BM, int BN>
+cudaError_t launch_tiles(const GemmArgs& a, int64_t batch, bool nt, cudaStream_t st) {
+  if (batch > 65535 || (a.M + BM - 1) / BM > 65535) return cudaErrorInvalidValue;
+  constexpr int T = (BM / 32) * (BN / 32) * 32;
+  constexpr int SMEM = 2 * BK * ((BM + 8) + (BN + 8)) * 8;
+  const dim3 grid((unsigned)((a.N + BN - 1) / BN), (unsigned)((a.M + BM - 1) / BM), (unsigned)batch);
+  auto kern = nt ? dgemm_kernel<BM, BN, true> : dgemm_kernel<BM, BN, false>;
+  if (SMEM > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e != cudaSuccess) return e;
+  }
+  kern<<<grid, T, SMEM, st>>>(a);
+  return cudaGetLastError();
+}
+
+// cfg: 1 = 64 x 64, 2 = 128 x 64, 3 = 64 x 128, 4 = 128 x 128 tiles; 0 = by shape
+cudaError_t launch_dgemm_cfg(const GemmArgs& a, int64_t batch, bool nt, cudaStream_t st, int cfg) {
+  if (cfg == 0) cfg = a.K <= 256 ? 2 : 1;
+  switch (cfg) {
+    case 1: return launch_tiles<64, 64>(a, batch, nt, st);
+    case 2: return launch_tiles<128, 64>(a, batch, nt, st);
+    case 3: return launch_tiles<64, 128>(a, batch, nt, st);
+    default: return launch_tiles<128, 128>(a, batch, nt, st);
   }
 }
 
@@ -160,12 +210,8 @@ cudaError_t launch_dgemm(int64_t batch, int64_t M, int64_t N, int64_t K, const d
                          int64_t strideA, const double* B, int64_t ldb, int64_t strideB, bool b_transposed,
                          double* C, int64_t ldc, int64_t strideC, cudaStream_t st) {
   if (batch <= 0 || M <= 0 || N <= 0) return cudaSuccess;
-  if (batch > 65535 || (M + BM - 1) / BM > 65535) return cudaErrorInvalidValue;
   GemmArgs a{M, N, K, A, lda, strideA, B, ldb, strideB, C, ldc, strideC};
-  const dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)batch);
-  if (b_transposed) dgemm_kernel<true><<<grid, GT, 0, st>>>(a);
-  else dgemm_kernel<false><<<grid, GT, 0, st>>>(a);
-  return cudaGetLastError();
+  return launch_dgemm_cfg(a, batch, b_transposed, st, 0);
 }
 
 }  // namespace rsa

@@ -6,15 +6,18 @@
 // text keys per (possibly ragged) text block; pooling_error (masks.py:165-171)
 // needs the deficits sum - len * mean.
 //
-// Layout: one CTA per (block, segment, head); 256 threads stream the block's
-// rows with 128-bit non-allocating loads (8 bf16 / 4 f32 / 2 f64 per load),
-// each thread owning a column chunk and a row phase.  For bf16/f32 data the
-// sums are plain fp64 adds, proven exact per block from its magnitude range
-// (see pass 1 below); otherwise (f64 data, or a block spanning too many
-// binades) partial sums are (hi, lo) TwoSum pairs.  Either way the merged
-// result is the exactly rounded sum, i.e. bit-identical to math.fsum, and
-// independent of launch geometry.
+// Two kernels.  bf16 (the model path): pool_bulk_kernel below, TMA-streamed.
+// f32 / f64 (the reference's own precisions) and unaligned bf16: pool_kernel,
+// one CTA per (block, segment, head); 256 threads stream the block's rows with
+// 128-bit non-allocating loads, each thread owning a column chunk and a row
+// phase.  For bf16/f32 data the sums are plain fp64 adds, proven exact per
+// block from its magnitude range (see pass 1 below); otherwise (f64 data, or a
+// block spanning too many binades) each column is summed by Shewchuk's
+// algorithm (fsum_exact).  Either way the result is the exactly rounded sum,
+// bit-identical to math.fsum, and independent of launch geometry.
 #include "rsa_internal.cuh"
+#include "tc_ptx.cuh"
+#include "tmap.cuh"
 
 #include <cfloat>
 
@@ -25,10 +28,41 @@ namespace {
 
 constexpr int kThreads = 256;
 
-__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
-  s = a + b;
-  double bb = s - a;
-  e = (a - (s - bb)) + (b - bb);
+// Shewchuk's exactly rounded sum (CPython math.fsum, including its half-even
+// correction) of n finite doubles at(0..n-1).
+template <typename F>
+__device__ double fsum_exact(int64_t n, F at) {
+  double p[48];   // non-overlapping partials, increasing magnitude (<= 40 for doubles)
+  int np = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    double x = at(i);
+    int j = 0;
+    for (int k = 0; k < np; ++k) {
+      double y = p[k];
+      if (fabs(x) < fabs(y)) { const double t = x; x = y; y = t; }
+      const double hi = __dadd_rn(x, y);
+      const double lo = __dsub_rn(y, __dsub_rn(hi, x));
+      if (lo != 0.0) p[j++] = lo;
+      x = hi;
+    }
+    p[j] = x;
+    np = j + 1;
+  }
+  if (np == 0) return 0.0;
+  int n2 = np;
+  double hi = p[--n2], lo = 0.0;
+  while (n2 > 0) {
+    const double x = hi, y = p[--n2];
+    hi = __dadd_rn(x, y);
+    const double yr = __dsub_rn(hi, x);
+    lo = __dsub_rn(y, yr);
+    if (lo != 0.0) break;
+  }
+  if (n2 > 0 && ((lo < 0.0 && p[n2 - 1] < 0.0) || (lo > 0.0 && p[n2 - 1] > 0.0))) {
+    const double y = __dmul_rn(lo, 2.0), x = __dadd_rn(hi, y);
+    if (y == __dsub_rn(x, hi)) hi = x;
+  }
+  return hi;
 }
 
 template <typename T, int VEC>
@@ -77,7 +111,6 @@ pool_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restric
   const T* src = (seg == 0 ? q : seg == 1 ? k : v) + (h * g.T + row0) * d;
 
   __shared__ double s_hi[2048];
-  __shared__ double s_lo[2048];
 
   const int tpr = (int)(d / VEC);          // threads per row
   const int rg_count = kThreads / tpr;     // row phases
@@ -164,31 +197,17 @@ pool_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restric
     __syncthreads();
     exact = s_exact != 0;
   }
-  if (!exact) {
-    double hi[VEC], lo[VEC];
+  if (!exact && rg < rg_count) {
+    // (the column sums come from fsum_exact below; this pass flags non-finite
+    // values and, for f64 data, copies the raw text keys)
+    for (int64_t r = rg; r < len; r += rg_count) {
+      double x[VEC];
+      load_vec<T, VEC>(src + r * d + c * VEC, x);
 #pragma unroll
-    for (int i = 0; i < VEC; ++i) { hi[i] = 0.0; lo[i] = 0.0; }
-    if (rg < rg_count) {
-      for (int64_t r = rg; r < len; r += rg_count) {
-        double x[VEC];
-        load_vec<T, VEC>(src + r * d + c * VEC, x);
+      for (int i = 0; i < VEC; ++i) nonfinite |= !(fabs(x[i]) <= DBL_MAX);
+      if (raw_out && !kTryPlain) {
 #pragma unroll
-        for (int i = 0; i < VEC; ++i) {
-          nonfinite |= !(fabs(x[i]) <= DBL_MAX);
-          double sm, e;
-          two_sum(hi[i], x[i], sm, e);
-          hi[i] = sm;
-          lo[i] += e;
-        }
-        if (raw_out && !kTryPlain) {
-#pragma unroll
-          for (int i = 0; i < VEC; ++i) raw_out[r * d + c * VEC + i] = x[i];
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < VEC; ++i) {
-        s_hi[rg * d + i * tpr + c] = hi[i];
-        s_lo[rg * d + i * tpr + c] = lo[i];
+        for (int i = 0; i < VEC; ++i) raw_out[r * d + c * VEC + i] = x[i];
       }
     }
   }
@@ -202,14 +221,8 @@ pool_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restric
       sum = 0.0;   // exact partial sums: plain adds stay exact (same bound)
       for (int p = 0; p < rg_count; ++p) sum += s_hi[p * d + slot];
     } else {
-      double S = 0.0, E = 0.0;
-      for (int p = 0; p < rg_count; ++p) {
-        double s, e;
-        two_sum(S, s_hi[p * d + slot], s, e);
-        S = s;
-        E += e + s_lo[p * d + slot];
-      }
-      sum = S + E;                            // exactly rounded block sum
+      // correctly rounded (math.fsum) column sum, one thread per column
+      sum = fsum_exact(len, [&](int64_t r) { return to_f64(src[r * d + col]); });
     }
     const double flen = (double)len;
     const double mean = sum / flen;           // core.py:172 fsum(...) / length
@@ -230,46 +243,37 @@ pool_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restric
 }
 
 // ---------------------------------------------------------------------------
-// bf16 fast path: persistent CTAs stream whole blocks (B rows x d bf16, one
-// contiguous B*d*2-byte range of [H][T][d]) into a shared-memory ring with 1-D
-// bulk async copies (cp.async.bulk, TMA engine), several blocks in flight per
-// CTA, and reduce them from shared memory.  The exactness argument is the one
-// of pool_kernel (pass 1): bf16 values have p = 8 significant bits, so fp64
-// partial sums are exact while e_max - e_min + 8 + ceil(log2 len) < 53; a
-// block that fails the test (never for sane data) is re-summed from the same
-// shared-memory copy with TwoSum pairs.  Bit-identical to math.fsum either way.
+// bf16 path: persistent CTAs (2 per SM) walk the pooling items -- one
+// (head, segment, block) = B rows x d bf16 -- and stream each into a
+// shared-memory ring with ONE TMA tensor load (a [d x B] box of the 4-D row
+// map, so any row strides work), STAGES items in flight per CTA.  Per item:
+//  phase A (all threads; 8 columns x B/RP rows each, 16-byte shared loads):
+//    every bf16 x is re-encoded EXACTLY as the fp64 value x * 2^-896 with two
+//    or three integer ops -- its f32 bit pattern shifted right by 3 with the
+//    sign kept: the 8-bit exponent lands in the low bits of the f64 exponent,
+//    the 7 significand bits at the top of the f64 significand; 0 -> +-0,
+//    subnormals -> f64 subnormals, one scale for all -- instead of a
+//    bf16->f64 conversion per element on the XU pipe (what bound round 1's
+//    kernel); fp64 adds; packed 16x2 integer max / min of the |x| bit
+//    patterns (3-input DPX min/max).  Lanes sharing columns merge by shuffle;
+//    one barrier.
+//  decision (every thread): the plain sums are exact iff
+//    e_max - e_min + 8 + ceil(log2 len) < 53 (e_min over nonzero values: a
+//    thread that saw an exact zero recomputes its minimum without zeros);
+//  phase B (d threads): the column's 8 warp partials, unscaled by 2^896
+//    (exact), mean / deficit.  A block failing the test (never for sane data)
+//    is re-summed per column with Shewchuk's algorithm -- the algorithm of
+//    math.fsum, correctly rounded -- from the same shared-memory copy.
+// Result: bit-identical to the reference's math.fsum pooling (core.py:154-189).
 // ---------------------------------------------------------------------------
 constexpr int kBulkThreads = 256;
 
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          (uint32_t)__cvta_generic_to_shared(dst)),
-      "l"(src), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(bar))
-      : "memory");
+// f32 bit pattern of a bf16 value (low 16 bits zero) -> the fp64 x * 2^-896, exactly
+__device__ __forceinline__ double bf16_scaled(uint32_t f32_bits) {
+  return __hiloint2double((int)(((int)f32_bits >> 3) & 0x8FFFE000), 0);
 }
-__device__ __forceinline__ void bar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
-               "r"(count)
-               : "memory");
-}
-__device__ __forceinline__ void bar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                   (uint32_t)__cvta_generic_to_shared(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(parity)
-        : "memory");
-  }
+__device__ __forceinline__ double unscale_896(double x) {
+  return __dmul_rn(x, __hiloint2double(0x77F00000, 0));   // * 2^896
 }
 
 struct PoolItem {
@@ -290,194 +294,191 @@ __device__ __forceinline__ PoolItem pool_item(const Geometry& g, int64_t i) {
 }
 
 template <int D, int STAGES>
-__global__ void __launch_bounds__(kBulkThreads, 3)
-pool_bulk_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k,
-                 const __nv_bfloat16* __restrict__ v, Workspace ws, Geometry g, int64_t n_items,
-                 const int32_t* __restrict__ perm, __nv_bfloat16* kp, __nv_bfloat16* vp,
-                 __nv_bfloat16* qp) {
-  constexpr int WPR = D / 2;                   // 32-bit words (bf16 pairs) per row
-  constexpr int RP = kBulkThreads / WPR;       // row phases
+__global__ void __launch_bounds__(kBulkThreads, 2)
+pool_bulk_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                 const __grid_constant__ CUtensorMap tm_v, const __nv_bfloat16* __restrict__ q,
+                 const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v, Workspace ws,
+                 Geometry g, int64_t n_items, const int32_t* __restrict__ perm, __nv_bfloat16* kp,
+                 __nv_bfloat16* vp, __nv_bfloat16* qp) {
+  constexpr int TPR = D / 8;                   // threads per row: 16 bytes (8 bf16) each
+  constexpr int RP = kBulkThreads / TPR;       // row phases
+  constexpr int WARPS = kBulkThreads / 32;
   extern __shared__ __align__(128) uint8_t smem[];
   const int stage_bytes = (int)(g.B * D * 2);
   uint8_t* ring = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * stage_bytes);
-  double* s_part = reinterpret_cast<double*>(full + STAGES);     // [RP][D] hi (+ [RP][D] lo)
-  float* s_rng = reinterpret_cast<float*>(s_part + 2 * RP * D);  // [8 warps][2]
-  __shared__ int s_exact;
+  double* s_part = reinterpret_cast<double*>(full + STAGES);        // [2][WARPS][D]
+  uint32_t* s_rng = reinterpret_cast<uint32_t*>(s_part + 2 * WARPS * D);   // [2][WARPS][2]
 
-  const int t = threadIdx.x;
-  const int word = t % WPR, rp = t / WPR;
-  auto src_of = [&](const PoolItem& it, uint32_t& bytes) -> const void* {
-    const int64_t len = kv_len(g, it.blk);
-    bytes = (uint32_t)(len * D * 2);
-    const __nv_bfloat16* base = it.seg == 0 ? q : it.seg == 1 ? k : v;
-    return base + (it.h * g.T + kv_row0(g, it.blk)) * D;
-  };
+  const int t = threadIdx.x, lane = t % 32, warp = t / 32;
+  const int tc = t % TPR, rp = t / TPR;
   if (t == 0) {
-    for (int s = 0; s < STAGES; ++s) bar_init(full + s, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    ptx::prefetch_tmap(&tm_q);
+    ptx::prefetch_tmap(&tm_k);
+    ptx::prefetch_tmap(&tm_v);
+    for (int st = 0; st < STAGES; ++st) ptx::mbar_init(full + st, 1);
+    ptx::fence_barrier_init();
   }
   __syncthreads();
-  // Stage item i into ring slot s (thread 0): one contiguous bulk copy.
-  auto fetch = [&](int64_t i, int s) {
+  // item i -> ring stage st (thread 0): one TMA box of B rows (rows past the
+  // block -- the next block, or zero fill past T -- are ignored)
+  auto fetch = [&](int64_t i, int st) {
     const PoolItem it = pool_item(g, i);
-    uint32_t bytes;
-    const void* src = src_of(it, bytes);
-    uint8_t* dst = ring + s * stage_bytes;
-    if (t == 0) {
-      bar_expect_tx(full + s, bytes);
-      bulk_g2s(dst, src, bytes, full + s);
-    }
+    ptx::mbar_expect_tx(full + st, (uint32_t)stage_bytes);
+    ptx::tma_load_4d(ring + st * stage_bytes, it.seg == 0 ? &tm_q : it.seg == 1 ? &tm_k : &tm_v, full + st, 0,
+                     (int)kv_row0(g, it.blk), (int)(it.h % g.hb), (int)(it.h / g.hb));
   };
-  // Permuted problem: every thread gathers 16-byte pieces of the block's rows
-  // (LDGSTS, cp.async groups) -- 128 row-sized bulk copies per block keep the
-  // TMA engine busy issuing instead of moving bytes.
-  constexpr int CPR = D * 2 / 16;   // 16-byte pieces per row
-  auto fetch_rows = [&](int64_t i, int s) {
+  // permuted (Morton) problem: every thread gathers 16-byte pieces of the
+  // block's rows (cp.async groups)
+  constexpr int CPR = D * 2 / 16;
+  auto fetch_rows = [&](int64_t i, int st) {
     const PoolItem it = pool_item(g, i);
     const int64_t len = kv_len(g, it.blk);
-    const __nv_bfloat16* base = (it.seg == 0 ? q : it.seg == 1 ? k : v) + it.h * g.T * D;
-    uint8_t* dst = ring + s * stage_bytes;
+    const __nv_bfloat16* base = it.seg == 0 ? q : it.seg == 1 ? k : v;
+    uint8_t* dst = ring + st * stage_bytes;
     for (int64_t c = t; c < len * CPR; c += kBulkThreads) {
       const int64_t r = c / CPR, cc = c % CPR;
       const int64_t row = it.blk < g.N ? perm[it.blk * g.B + r] : kv_row0(g, it.blk) + r;
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
                        (uint32_t)__cvta_generic_to_shared(dst + r * D * 2 + cc * 16)),
-                   "l"(base + row * D + cc * 8)
+                   "l"(base + row_off(g, it.h, row) + cc * 8)
                    : "memory");
     }
   };
   if (perm) {
-    for (int s = 0; s < STAGES; ++s) {
-      const int64_t i = blockIdx.x + (int64_t)s * gridDim.x;
-      if (i < n_items) fetch_rows(i, s);
+    for (int st = 0; st < STAGES; ++st) {
+      const int64_t i = blockIdx.x + (int64_t)st * gridDim.x;
+      if (i < n_items) fetch_rows(i, st);
       asm volatile("cp.async.commit_group;" ::: "memory");   // one group per stage, even if empty
     }
-  } else if (t < 32) {
-    for (int s = 0; s < STAGES; ++s) {
-      const int64_t i = blockIdx.x + (int64_t)s * gridDim.x;
-      if (i >= n_items) break;
-      fetch(i, s);
+  } else if (t == 0) {
+    for (int st = 0; st < STAGES; ++st) {
+      const int64_t i = blockIdx.x + (int64_t)st * gridDim.x;
+      if (i < n_items) fetch(i, st);
     }
   }
   int64_t kk = 0;
   for (int64_t i = blockIdx.x; i < n_items; i += gridDim.x, ++kk) {
-    const int s = (int)(kk % STAGES);
+    const int st = (int)(kk % STAGES);
+    const int buf = (int)(kk & 1);
     const PoolItem it = pool_item(g, i);
     const int64_t len = kv_len(g, it.blk);
     if (perm) {
-      // this item's group (committed STAGES groups ago) has landed, all threads' pieces
       asm volatile("cp.async.wait_group %0;" ::"n"(STAGES - 1) : "memory");
       __syncthreads();
     } else {
-      bar_wait(full + s, (uint32_t)((kk / STAGES) & 1));
+      ptx::mbar_wait(full + st, (uint32_t)((kk / STAGES) & 1));
     }
-    const uint32_t* blk = reinterpret_cast<const uint32_t*>(ring + s * stage_bytes);
+    const uint8_t* blk = ring + st * stage_bytes;
     if (kp && (it.seg > 0 || qp) && t == 0) {
       if (perm) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> bulk read
-      // the permuted Q / K / V block, contiguous, for K3's TMA (shared -> global bulk copy)
+      // the permuted Q / K / V block, contiguous [H][T][d], for K3's TMA
       __nv_bfloat16* dstp = (it.seg == 0 ? qp : it.seg == 1 ? kp : vp) + (it.h * g.T + kv_row0(g, it.blk)) * D;
       asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n\t"
                    "cp.async.bulk.commit_group;" ::"l"(dstp),
                    "r"((uint32_t)__cvta_generic_to_shared(blk)), "r"((uint32_t)(len * D * 2))
                    : "memory");
     }
-    // pass 1: plain fp64 sums of this thread's column pair over its row phase,
-    // plus the magnitude range (bf16 bits & 0x7FFF is monotonic in |x|)
-    double a0 = 0.0, a1 = 0.0;
-    // packed 16x2 magnitude tracking: max of (bits & 0x7FFF); min over
-    // nonzero values through the key (mag + 0x7FFF) & 0x7FFF (0 -> 0x7FFF,
-    // x -> x - 1; no carry crosses the halves)
-    uint32_t pmax = 0, pmin = 0x7FFF7FFFu;
+    // ---- phase A ----
     const bool text_k = (it.seg == 1) && (it.blk >= g.N);
     double* raw_out = text_k ? ws.k_cat + (it.h * g.n_cols + g.N + (kv_row0(g, it.blk) - g.Tv)) * D : nullptr;
-#pragma unroll 8
+    double acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+    uint32_t pmax = 0, pmin = 0x7FFF7FFFu;
+#pragma unroll 4
     for (int64_t r = rp; r < len; r += RP) {
-      const uint32_t w = blk[r * WPR + word];
-      const float x0 = __uint_as_float(w << 16), x1 = __uint_as_float(w & 0xFFFF0000u);
-      a0 += (double)x0;
-      a1 += (double)x1;
-      const uint32_t mag = w & 0x7FFF7FFFu;
-      pmax = __vmaxu2(pmax, mag);
-      pmin = __vminu2(pmin, (mag + 0x7FFF7FFFu) & 0x7FFF7FFFu);
+      const uint4 w4 = *reinterpret_cast<const uint4*>(blk + r * D * 2 + tc * 16);
+      const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        acc[2 * j] += bf16_scaled(w[j] << 16);
+        acc[2 * j + 1] += bf16_scaled(w[j]);   // (the low half is masked off by the encoding)
+      }
+      const uint32_t m0 = w4.x & 0x7FFF7FFFu, m1 = w4.y & 0x7FFF7FFFu, m2 = w4.z & 0x7FFF7FFFu,
+                     m3 = w4.w & 0x7FFF7FFFu;
+      pmax = __vimax3_u16x2(pmax, __vimax3_u16x2(m0, m1, m2), m3);
+      pmin = __vimin3_u16x2(pmin, __vimin3_u16x2(m0, m1, m2), m3);
       if (raw_out) {
-        raw_out[r * D + 2 * word] = (double)x0;
-        raw_out[r * D + 2 * word + 1] = (double)x1;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          raw_out[r * D + tc * 8 + 2 * j] = (double)__uint_as_float(w[j] << 16);
+          raw_out[r * D + tc * 8 + 2 * j + 1] = (double)__uint_as_float(w[j] & 0xFFFF0000u);
+        }
       }
     }
-    s_part[rp * D + 2 * word] = a0;
-    s_part[rp * D + 2 * word + 1] = a1;
-    uint32_t bmax = max(pmax & 0xFFFFu, pmax >> 16);
-    const uint32_t kmin = min(pmin & 0xFFFFu, pmin >> 16);
-    uint32_t bmin = kmin == 0x7FFFu ? 0xFFFFu : kmin + 1;   // 0xFFFF: no nonzero value
+    uint32_t tmax = max(pmax & 0xFFFFu, pmax >> 16);
+    uint32_t tmin = min(pmin & 0xFFFFu, pmin >> 16);
+    if (tmin == 0) {
+      // an exact zero: the minimum over NONZERO magnitudes (0 -> 0x7FFF key)
+      uint32_t kmin = 0x7FFF7FFFu;
+      for (int64_t r = rp; r < len; r += RP) {
+        const uint4 w4 = *reinterpret_cast<const uint4*>(blk + r * D * 2 + tc * 16);
+        const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) kmin = __vminu2(kmin, ((w[j] & 0x7FFF7FFFu) + 0x7FFF7FFFu) & 0x7FFF7FFFu);
+      }
+      const uint32_t km = min(kmin & 0xFFFFu, kmin >> 16);
+      tmin = km == 0x7FFFu ? 0xFFFFu : km + 1;   // 0xFFFF: no nonzero value
+    }
+    // lanes holding the same 8 columns (other row phases) merge their sums
+#pragma unroll
+    for (int o = TPR; o < 32; o <<= 1)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      bmax = max(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
-      bmin = min(bmin, __shfl_xor_sync(0xffffffffu, bmin, o));
+      tmax = max(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+      tmin = min(tmin, __shfl_xor_sync(0xffffffffu, tmin, o));
     }
-    if (t % 32 == 0) {
-      reinterpret_cast<uint32_t*>(s_rng)[2 * (t / 32)] = bmax;
-      reinterpret_cast<uint32_t*>(s_rng)[2 * (t / 32) + 1] = bmin;
+    if (lane < TPR) {
+      double2* dst = reinterpret_cast<double2*>(s_part + (buf * WARPS + warp) * D + tc * 8);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dst[j] = make_double2(acc[2 * j], acc[2 * j + 1]);
     }
+    if (lane == 0) {
+      s_rng[(buf * WARPS + warp) * 2] = tmax;
+      s_rng[(buf * WARPS + warp) * 2 + 1] = tmin;
+    }
+    if (t == 0 && kp) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // permuted copy read out
     __syncthreads();
-    if (t == 0) {
-      uint32_t mx = 0, mn = 0xFFFFu;
-      for (int w = 0; w < kBulkThreads / 32; ++w) {
-        mx = max(mx, reinterpret_cast<uint32_t*>(s_rng)[2 * w]);
-        mn = min(mn, reinterpret_cast<uint32_t*>(s_rng)[2 * w + 1]);
-      }
-      if (mx >= 0x7F80u) atomicOr(ws.status + ST_NONFINITE, 1);   // exponent field 0xFF: inf / NaN
-      int lg = 0;
-      while ((int64_t(1) << lg) < len) ++lg;
-      // exponent fields (bits >> 7); subnormals (field 0) count as exponent 1
-      const int emax = max(1, (int)(mx >> 7)), emin = max(1, (int)(mn >> 7));
-      s_exact = (mn == 0xFFFFu) || (emax - emin + 8 + lg < 53);
+    // ---- decision (uniform) ----
+    uint32_t mx = 0, mn = 0xFFFFu;
+#pragma unroll
+    for (int w2 = 0; w2 < WARPS; ++w2) {
+      mx = max(mx, s_rng[(buf * WARPS + w2) * 2]);
+      mn = min(mn, s_rng[(buf * WARPS + w2) * 2 + 1]);
     }
-    __syncthreads();
-    const bool exact = s_exact != 0;
+    if (t == 0 && mx >= 0x7F80u) atomicOr(ws.status + ST_NONFINITE, 1);   // exponent field 0xFF: inf / NaN
+    const int lg = len > 1 ? 32 - __clz((int)(len - 1)) : 0;
+    // exponent fields (bits >> 7); subnormals (field 0) count as exponent 1
+    const int emax = max(1, (int)(mx >> 7)), emin = max(1, (int)(mn >> 7));
+    const bool exact = (mn == 0xFFFFu) || (emax - emin + 8 + lg < 53);
+    double sum = 0.0;
     if (!exact) {
-      // TwoSum (hi, lo) pairs over the same shared-memory copy
-      double h0 = 0.0, l0 = 0.0, h1 = 0.0, l1 = 0.0;
-      for (int64_t r = rp; r < len; r += RP) {
-        const uint32_t w = blk[r * WPR + word];
-        double sm, e;
-        two_sum(h0, (double)__uint_as_float(w << 16), sm, e); h0 = sm; l0 += e;
-        two_sum(h1, (double)__uint_as_float(w & 0xFFFF0000u), sm, e); h1 = sm; l1 += e;
+      if (t < D)
+        sum = fsum_exact(len, [&](int64_t r) {
+          return (double)__bfloat162float(reinterpret_cast<const __nv_bfloat16*>(blk)[r * D + t]);
+        });
+      __syncthreads();   // every column has been read from the stage
+    }
+    // ---- refill stage st with this CTA's item STAGES ahead ----
+    {
+      const int64_t nx = i + (int64_t)STAGES * gridDim.x;
+      if (perm) {
+        if (nx < n_items) fetch_rows(nx, st);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      } else if (t == 0 && nx < n_items) {
+        fetch(nx, st);
       }
-      s_part[rp * D + 2 * word] = h0;
-      s_part[rp * D + 2 * word + 1] = h1;
-      s_part[RP * D + rp * D + 2 * word] = l0;
-      s_part[RP * D + rp * D + 2 * word + 1] = l1;
-      __syncthreads();
     }
-    // stage s is free (its permuted copy, if any, has been read out): refill
-    // it with this CTA's item STAGES ahead
-    if (perm) {
-      if (t == 0 && kp) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      __syncthreads();
-      const int64_t nx = i + (int64_t)STAGES * gridDim.x;
-      if (nx < n_items) fetch_rows(nx, s);
-      asm volatile("cp.async.commit_group;" ::: "memory");
-    } else if (t < 32) {
-      if (t == 0 && kp) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      __syncwarp();
-      const int64_t nx = i + (int64_t)STAGES * gridDim.x;
-      if (nx < n_items) fetch(nx, s);
-    }
-    for (int col = t; col < D; col += kBulkThreads) {
-      double sum;
+    // ---- phase B ----
+    if (t < D) {
+      const int col = t;
       if (exact) {
-        sum = 0.0;
-        for (int p = 0; p < RP; ++p) sum += s_part[p * D + col];
-      } else {
-        double S = 0.0, E = 0.0;
-        for (int p = 0; p < RP; ++p) {
-          double sm, e;
-          two_sum(S, s_part[p * D + col], sm, e);
-          S = sm;
-          E += e + s_part[RP * D + p * D + col];
-        }
-        sum = S + E;
+#pragma unroll
+        for (int w2 = 0; w2 < WARPS; ++w2) sum += s_part[(buf * WARPS + w2) * D + col];
+        sum = unscale_896(sum);
       }
       const double flen = (double)len;
       const double mean = sum / flen;            // core.py:172 fsum(...) / length
@@ -495,7 +496,6 @@ pool_bulk_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
       }
       if (it.seg < 2 && deficit != 0.0) atomicOr(ws.status + ST_DEFICIT, 1);
     }
-    __syncthreads();
   }
   if (t == 0 && kp) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
@@ -503,9 +503,14 @@ pool_bulk_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __res
 template <int D>
 cudaError_t launch_bulk(const Geometry& g, const void* q, const void* k, const void* v, const Workspace& ws,
                         cudaStream_t st, const int32_t* perm, void* kp, void* vp, void* qp) {
-  constexpr int STAGES = 2;
-  constexpr int RP = kBulkThreads / (D / 2);
-  const size_t smem = (size_t)STAGES * g.B * D * 2 + STAGES * 8 + 2 * RP * D * 8 + 64;
+  constexpr int STAGES = 3;
+  constexpr int WARPS = kBulkThreads / 32;
+  const size_t smem = (size_t)STAGES * g.B * D * 2 + STAGES * 8 + 2 * WARPS * D * 8 + 2 * WARPS * 2 * 4;
+  CUtensorMap tq, tk, tv;
+  if (!make_rows_tmap(&tq, q, g, D, (int)g.B, CU_TENSOR_MAP_SWIZZLE_NONE) ||
+      !make_rows_tmap(&tk, k, g, D, (int)g.B, CU_TENSOR_MAP_SWIZZLE_NONE) ||
+      !make_rows_tmap(&tv, v, g, D, (int)g.B, CU_TENSOR_MAP_SWIZZLE_NONE))
+    return cudaErrorInvalidValue;
   auto kern = pool_bulk_kernel<D, STAGES>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -513,8 +518,8 @@ cudaError_t launch_bulk(const Geometry& g, const void* q, const void* k, const v
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t n_items = g.H * (g.N + 2 * g.M);
-  const int64_t grid = std::min<int64_t>(n_items, (int64_t)sms * 3);
-  kern<<<(unsigned)grid, kBulkThreads, smem, st>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
+  const int64_t grid = std::min<int64_t>(n_items, (int64_t)sms * 2);
+  kern<<<(unsigned)grid, kBulkThreads, smem, st>>>(tq, tk, tv, (const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
                                                    (const __nv_bfloat16*)v, ws, g, n_items, perm,
                                                    (__nv_bfloat16*)kp, (__nv_bfloat16*)vp, (__nv_bfloat16*)qp);
   return cudaGetLastError();
@@ -546,7 +551,9 @@ cudaError_t launch_pool(const Geometry& g, const void* q, const void* k, const v
       // bulk-copy streaming path when a block is one 16-byte-aligned range
       // that fits two ring stages per CTA, three CTAs per SM
       const bool aligned = ((uintptr_t)q % 16 == 0) && ((uintptr_t)k % 16 == 0) && ((uintptr_t)v % 16 == 0);
-      const bool fits = g.B * g.d * 2 * 2 <= 64 * 1024;
+      // rows 16-byte aligned for TMA; three ring stages + partials fit two CTAs per SM
+      const bool fits = g.B * g.d * 2 * 3 <= 96 * 1024 && g.B <= 256 && (g.s_tok * 2) % 16 == 0 &&
+                        (g.s_head * 2) % 16 == 0 && (g.s_batch * 2) % 16 == 0;
       if (aligned && fits && g.d == 128) return launch_bulk<128>(g, q, k, v, ws, st, perm, kp, vp, qp);
       if (aligned && fits && g.d == 64) return launch_bulk<64>(g, q, k, v, ws, st, perm, kp, vp, qp);
       if (perm) return cudaErrorNotSupported;

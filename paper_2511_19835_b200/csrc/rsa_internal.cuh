@@ -46,7 +46,16 @@ struct Geometry {
   // video block (opt-in extension; the reference
   // raises BlockSizeError, core.py:71-72)
   int64_t q_last;
+  // element strides of the rows of Q, K, V and O (d contiguous): head h is
+  // batch entry h / hb, head h % hb of it.  Contiguous [H][T][d]: hb = H,
+  // s_tok = d, s_head = T d, s_batch = H T d (rsa_shape without a layout).
+  int64_t hb, s_tok, s_head, s_batch;
 };
+
+// element offset of row `row` of head h
+__host__ __device__ __forceinline__ int64_t row_off(const Geometry& g, int64_t h, int64_t row) {
+  return (h / g.hb) * g.s_batch + (h % g.hb) * g.s_head + row * g.s_tok;
+}
 
 // tokens in video (query) block n
 __host__ __device__ __forceinline__ int64_t q_len(const Geometry& g, int64_t n) {
@@ -127,6 +136,6 @@ cudaError_t launch_permute_rows(const Geometry& g, const int32_t* perm, const vo
 cudaError_t launch_attn_tc(const Geometry& g, const void* q, const void* k, const void* v,
                            void* out, float* lse, const Workspace& ws, bool rectify,
                            bool text, cudaStream_t st, int* launches, const int32_t* perm = nullptr,
-                           const void* q_perm = nullptr);
+                           const void* q_perm = nullptr, int kernel = RSA_KERNEL_AUTO);
 
 }  // namespace rsa

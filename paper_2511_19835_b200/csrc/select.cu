@@ -869,13 +869,11 @@ cudaError_t launch_select(const Geometry& g, const rsa_config& cfg, int64_t k_fl
   while (p2 < g.M) p2 <<= 1;
   P.p2 = p2;
   P.use_sort = 0;   // radix select (a full bitonic sort of every row measured 2x slower)
-  // the register-resident kernel covers rows up to 16 * RT columns without the
-  // cumulative-weight rule (p > 0 needs the sorted cumsum); RSA_SELECT_REG=0 forces
-  // the general one (A/B)
-  static const int reg_env = [] { const char* e = getenv("RSA_SELECT_REG"); return e ? atoi(e) : 1; }();
+  // the register-resident kernel covers rows up to 16 * RT columns; wider
+  // rows take the general shared-memory kernel
   const int per = (int)((g.n_cols + RT - 1) / RT);
   const bool cum = P.p > 0.0;
-  const bool reg = reg_env != 0 && !P.use_sort && per <= 16;
+  const bool reg = !P.use_sort && per <= 16;
   if (reg) {
     size_t smem = (size_t)(g.n_cols + g.N + g.Tt + g.n_text) * 8 + (size_t)g.M + 16;
     if (cum) smem += 16 + (size_t)p2 * 12 + (size_t)g.M;
