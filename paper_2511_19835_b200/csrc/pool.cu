@@ -243,30 +243,26 @@ pool_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restric
 }
 
 // ---------------------------------------------------------------------------
-// bf16 path: persistent CTAs (2 per SM) walk the pooling items -- one
-// (head, segment, block) = B rows x d bf16 -- and stream each into a
-// shared-memory ring with ONE TMA tensor load (a [d x B] box of the 4-D row
-// map, so any row strides work), STAGES items in flight per CTA.  Per item:
-//  phase A (all threads; 8 columns x B/RP rows each, 16-byte shared loads):
-//    every bf16 x is re-encoded EXACTLY as the fp64 value x * 2^-896 with two
+// bf16 path (pool_warp_kernel below): every pooling item -- one (head,
+// segment, block) = B rows x d bf16 -- is reduced by ONE warp from a TMA-fed
+// shared-memory ring (a [d x SR] box of the 4-D row map, so any row strides
+// work).  Per element:
+//    the bf16 x is re-encoded EXACTLY as the fp64 value x * 2^-896 with two
 //    or three integer ops -- its f32 bit pattern shifted right by 3 with the
 //    sign kept: the 8-bit exponent lands in the low bits of the f64 exponent,
 //    the 7 significand bits at the top of the f64 significand; 0 -> +-0,
 //    subnormals -> f64 subnormals, one scale for all -- instead of a
 //    bf16->f64 conversion per element on the XU pipe (what bound round 1's
-//    kernel); fp64 adds; packed 16x2 integer max / min of the |x| bit
-//    patterns (3-input DPX min/max).  Lanes sharing columns merge by shuffle;
-//    one barrier.
-//  decision (every thread): the plain sums are exact iff
-//    e_max - e_min + 8 + ceil(log2 len) < 53 (e_min over nonzero values: a
-//    thread that saw an exact zero recomputes its minimum without zeros);
-//  phase B (d threads): the column's 8 warp partials, unscaled by 2^896
-//    (exact), mean / deficit.  A block failing the test (never for sane data)
-//    is re-summed per column with Shewchuk's algorithm -- the algorithm of
-//    math.fsum, correctly rounded -- from the same shared-memory copy.
+//    kernel); an fp64 add; packed 16x2 integer max / min of the |x| bit
+//    patterns (3-input DPX min/max).
+// Per item: lanes sharing columns merge by shuffle, the magnitude range by
+// warp REDUX; the plain sums are exact iff e_max - e_min + 8 + ceil(log2 len)
+// < 53 (e_min over nonzero values: a part with an exact zero recomputes its
+// minimum without zeros), and are then unscaled by 2^896 (exact).  A block
+// failing the test (never for sane data) is re-summed per column with
+// Shewchuk's algorithm -- the algorithm of math.fsum, correctly rounded.
 // Result: bit-identical to the reference's math.fsum pooling (core.py:154-189).
 // ---------------------------------------------------------------------------
-constexpr int kBulkThreads = 256;
 
 // f32 bit pattern of a bf16 value (low 16 bits zero) -> the fp64 x * 2^-896, exactly
 __device__ __forceinline__ double bf16_scaled(uint32_t f32_bits) {
@@ -277,251 +273,263 @@ __device__ __forceinline__ double unscale_896(double x) {
 }
 
 struct PoolItem {
-  int64_t h, blk;
-  int seg;
+  int h, blk, seg;
 };
 
-// items: per head [N Q video blocks][M K blocks][M V blocks]
-__device__ __forceinline__ PoolItem pool_item(const Geometry& g, int64_t i) {
-  const int64_t per_head = g.N + 2 * g.M;
+// items: per head [N Q video blocks][M K blocks][M V blocks] (32-bit: the
+// launcher checks H (N + 2M) < 2^31)
+__device__ __forceinline__ PoolItem pool_item(int per_head, int n_q, int n_kv, int i) {
   PoolItem it;
   it.h = i / per_head;
-  int64_t r = i % per_head;
-  if (r < g.N) { it.seg = 0; it.blk = r; }
-  else if (r < g.N + g.M) { it.seg = 1; it.blk = r - g.N; }
-  else { it.seg = 2; it.blk = r - g.N - g.M; }
+  const int r = i - it.h * per_head;
+  if (r < n_q) { it.seg = 0; it.blk = r; }
+  else if (r < n_q + n_kv) { it.seg = 1; it.blk = r - n_q; }
+  else { it.seg = 2; it.blk = r - n_q - n_kv; }
   return it;
 }
 
-template <int D, int STAGES>
-__global__ void __launch_bounds__(kBulkThreads, 2)
-pool_bulk_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+// One warp per CTA, one pooling item (block) at a time, no block-wide
+// synchronisation: the warp's lane 0 streams the item in 8 KB parts (a TMA
+// box of SR rows; four parts per 32 KB block) through a 2-stage ring of its
+// own, the 32 lanes reduce every part as it lands (lanes l and l + 16 take
+// alternate rows of the same 8 columns at d = 128), and the item's column sums,
+// exactness test (warp REDUX of the magnitude range) and outputs stay in the
+// warp.  Twelve such CTAs per SM keep 192 KB of HBM reads in flight (A/B over
+// part size x stages x CTAs/SM: 8 KB x 2 x 12 best).
+#ifndef RSA_K1_PART_BYTES
+#define RSA_K1_PART_BYTES 8192   // one TMA part (rows x d x 2 bytes)
+#endif
+#ifndef RSA_K1_CTAS_PER_SM
+#define RSA_K1_CTAS_PER_SM 12    // one warp each
+#endif
+#ifndef RSA_K1_STAGES
+#define RSA_K1_STAGES 2
+#endif
+
+template <int D>
+__global__ void __launch_bounds__(32, RSA_K1_CTAS_PER_SM)
+pool_warp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                  const __grid_constant__ CUtensorMap tm_v, const __nv_bfloat16* __restrict__ q,
                  const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v, Workspace ws,
-                 Geometry g, int64_t n_items, const int32_t* __restrict__ perm, __nv_bfloat16* kp,
+                 Geometry g, int n_items, int stage_rows, const int32_t* __restrict__ perm, __nv_bfloat16* kp,
                  __nv_bfloat16* vp, __nv_bfloat16* qp) {
-  constexpr int TPR = D / 8;                   // threads per row: 16 bytes (8 bf16) each
-  constexpr int RP = kBulkThreads / TPR;       // row phases
-  constexpr int WARPS = kBulkThreads / 32;
+  constexpr int TPR = D / 8;          // lanes per row: 16 bytes (8 bf16) each
+  constexpr int RPI = 32 / TPR;       // rows per warp iteration
+  constexpr int NST = RSA_K1_STAGES;
   extern __shared__ __align__(128) uint8_t smem[];
-  const int stage_bytes = (int)(g.B * D * 2);
-  uint8_t* ring = smem;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * stage_bytes);
-  double* s_part = reinterpret_cast<double*>(full + STAGES);        // [2][WARPS][D]
-  uint32_t* s_rng = reinterpret_cast<uint32_t*>(s_part + 2 * WARPS * D);   // [2][WARPS][2]
+  const int SR = stage_rows;
+  const int stage_bytes = SR * D * 2;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NST * stage_bytes);
+  const int lane = threadIdx.x, tc = lane % TPR, rl = lane / TPR;
+  const int n_q = (int)g.N, n_kv = (int)g.M, per_head = n_q + 2 * n_kv;
+  const int B = (int)g.B;
+  const int parts = (B + SR - 1) / SR;
+  const __nv_bfloat16* bases[3] = {q, k, v};
 
-  const int t = threadIdx.x, lane = t % 32, warp = t / 32;
-  const int tc = t % TPR, rp = t / TPR;
-  if (t == 0) {
+  // fetch cursor: (item, part) of the next stage load
+  int fi = blockIdx.x, fpart = 0;
+  constexpr int CPR = D * 2 / 16;
+  auto issue = [&](int st) {
+    if (fi >= n_items) return;
+    const PoolItem it = pool_item(per_head, n_q, n_kv, fi);
+    const int r0 = fpart * SR;
+    if (perm) {   // permuted (Morton) rows: every lane gathers 16-byte pieces (cp.async)
+      const int len = (int)kv_len(g, it.blk);
+      const int rows = min(SR, len - r0);
+      uint8_t* dst = smem + st * stage_bytes;
+      for (int c = lane; c < rows * CPR; c += 32) {
+        const int r = c / CPR, cc = c % CPR;
+        const int64_t row = it.blk < n_q ? perm[(int64_t)it.blk * B + r0 + r] : kv_row0(g, it.blk) + r0 + r;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(dst + r * D * 2 + cc * 16)),
+                     "l"(bases[it.seg] + row_off(g, it.h, row) + cc * 8)
+                     : "memory");
+      }
+    } else if (lane == 0) {
+      ptx::mbar_expect_tx(full + st, (uint32_t)stage_bytes);
+      ptx::tma_load_4d(smem + st * stage_bytes, it.seg == 0 ? &tm_q : it.seg == 1 ? &tm_k : &tm_v, full + st, 0,
+                       (int)kv_row0(g, it.blk) + r0, it.h % (int)g.hb, it.h / (int)g.hb);
+    }
+    if (++fpart == parts) { fpart = 0; fi += gridDim.x; }
+  };
+  if (lane == 0) {
     ptx::prefetch_tmap(&tm_q);
     ptx::prefetch_tmap(&tm_k);
     ptx::prefetch_tmap(&tm_v);
-    for (int st = 0; st < STAGES; ++st) ptx::mbar_init(full + st, 1);
+    for (int st = 0; st < NST; ++st) ptx::mbar_init(full + st, 1);
     ptx::fence_barrier_init();
   }
-  __syncthreads();
-  // item i -> ring stage st (thread 0): one TMA box of B rows (rows past the
-  // block -- the next block, or zero fill past T -- are ignored)
-  auto fetch = [&](int64_t i, int st) {
-    const PoolItem it = pool_item(g, i);
-    ptx::mbar_expect_tx(full + st, (uint32_t)stage_bytes);
-    ptx::tma_load_4d(ring + st * stage_bytes, it.seg == 0 ? &tm_q : it.seg == 1 ? &tm_k : &tm_v, full + st, 0,
-                     (int)kv_row0(g, it.blk), (int)(it.h % g.hb), (int)(it.h / g.hb));
-  };
-  // permuted (Morton) problem: every thread gathers 16-byte pieces of the
-  // block's rows (cp.async groups)
-  constexpr int CPR = D * 2 / 16;
-  auto fetch_rows = [&](int64_t i, int st) {
-    const PoolItem it = pool_item(g, i);
-    const int64_t len = kv_len(g, it.blk);
-    const __nv_bfloat16* base = it.seg == 0 ? q : it.seg == 1 ? k : v;
-    uint8_t* dst = ring + st * stage_bytes;
-    for (int64_t c = t; c < len * CPR; c += kBulkThreads) {
-      const int64_t r = c / CPR, cc = c % CPR;
-      const int64_t row = it.blk < g.N ? perm[it.blk * g.B + r] : kv_row0(g, it.blk) + r;
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                       (uint32_t)__cvta_generic_to_shared(dst + r * D * 2 + cc * 16)),
-                   "l"(base + row_off(g, it.h, row) + cc * 8)
-                   : "memory");
-    }
-  };
-  if (perm) {
-    for (int st = 0; st < STAGES; ++st) {
-      const int64_t i = blockIdx.x + (int64_t)st * gridDim.x;
-      if (i < n_items) fetch_rows(i, st);
-      asm volatile("cp.async.commit_group;" ::: "memory");   // one group per stage, even if empty
-    }
-  } else if (t == 0) {
-    for (int st = 0; st < STAGES; ++st) {
-      const int64_t i = blockIdx.x + (int64_t)st * gridDim.x;
-      if (i < n_items) fetch(i, st);
-    }
+  __syncwarp();
+  for (int st = 0; st < NST; ++st) {
+    issue(st);
+    if (perm) asm volatile("cp.async.commit_group;" ::: "memory");   // one group per stage, even if empty
   }
-  int64_t kk = 0;
-  for (int64_t i = blockIdx.x; i < n_items; i += gridDim.x, ++kk) {
-    const int st = (int)(kk % STAGES);
-    const int buf = (int)(kk & 1);
-    const PoolItem it = pool_item(g, i);
-    const int64_t len = kv_len(g, it.blk);
-    if (perm) {
-      asm volatile("cp.async.wait_group %0;" ::"n"(STAGES - 1) : "memory");
-      __syncthreads();
-    } else {
-      ptx::mbar_wait(full + st, (uint32_t)((kk / STAGES) & 1));
-    }
-    const uint8_t* blk = ring + st * stage_bytes;
-    if (kp && (it.seg > 0 || qp) && t == 0) {
-      if (perm) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> bulk read
-      // the permuted Q / K / V block, contiguous [H][T][d], for K3's TMA
-      __nv_bfloat16* dstp = (it.seg == 0 ? qp : it.seg == 1 ? kp : vp) + (it.h * g.T + kv_row0(g, it.blk)) * D;
-      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n\t"
-                   "cp.async.bulk.commit_group;" ::"l"(dstp),
-                   "r"((uint32_t)__cvta_generic_to_shared(blk)), "r"((uint32_t)(len * D * 2))
-                   : "memory");
-    }
-    // ---- phase A ----
-    const bool text_k = (it.seg == 1) && (it.blk >= g.N);
-    double* raw_out = text_k ? ws.k_cat + (it.h * g.n_cols + g.N + (kv_row0(g, it.blk) - g.Tv)) * D : nullptr;
+  int u = 0;   // stage loads consumed
+  for (int i = blockIdx.x; i < n_items; i += gridDim.x) {
+    const PoolItem it = pool_item(per_head, n_q, n_kv, i);
+    const int len = (int)kv_len(g, it.blk);
+    const bool text_k = it.seg == 1 && it.blk >= n_q;
     double acc[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[j] = 0.0;
-    uint32_t pmax = 0, pmin = 0x7FFF7FFFu;
-#pragma unroll 4
-    for (int64_t r = rp; r < len; r += RP) {
-      const uint4 w4 = *reinterpret_cast<const uint4*>(blk + r * D * 2 + tc * 16);
-      const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        acc[2 * j] += bf16_scaled(w[j] << 16);
-        acc[2 * j + 1] += bf16_scaled(w[j]);   // (the low half is masked off by the encoding)
+    // packed 16x2 |x| bit patterns: max, and min over NONZERO values (0xFFFF: none)
+    uint32_t pmax = 0, nzmin = 0xFFFFFFFFu;
+    for (int part = 0; part < parts; ++part, ++u) {
+      const int st = u % NST;
+      if (perm) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(NST - 1) : "memory");
+        __syncwarp();
+      } else {
+        ptx::mbar_wait(full + st, (uint32_t)((u / NST) & 1));
       }
-      const uint32_t m0 = w4.x & 0x7FFF7FFFu, m1 = w4.y & 0x7FFF7FFFu, m2 = w4.z & 0x7FFF7FFFu,
-                     m3 = w4.w & 0x7FFF7FFFu;
-      pmax = __vimax3_u16x2(pmax, __vimax3_u16x2(m0, m1, m2), m3);
-      pmin = __vimin3_u16x2(pmin, __vimin3_u16x2(m0, m1, m2), m3);
-      if (raw_out) {
+      const uint8_t* stage = smem + st * stage_bytes;
+      const int r0 = part * SR;
+      const int rows = min(SR, len - r0);   // (<= 0: a short block's unused part)
+      if (kp && (it.seg > 0 || qp) && lane == 0 && rows > 0) {
+        if (perm) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> bulk read
+        // the permuted Q / K / V rows, contiguous [H][T][d], for K3's TMA
+        __nv_bfloat16* dstp =
+            (it.seg == 0 ? qp : it.seg == 1 ? kp : vp) + ((int64_t)it.h * g.T + kv_row0(g, it.blk) + r0) * D;
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n\t"
+                     "cp.async.bulk.commit_group;" ::"l"(dstp),
+                     "r"((uint32_t)__cvta_generic_to_shared(stage)), "r"((uint32_t)(rows * D * 2))
+                     : "memory");
+      }
+      uint32_t pmin = 0xFFFFFFFFu;   // this part's min, zeros included
+      const uint8_t* rowp = stage + rl * D * 2 + tc * 16;
+#pragma unroll 4
+      for (int r = rl; r < rows; r += RPI, rowp += RPI * D * 2) {
+        const uint4 w4 = *reinterpret_cast<const uint4*>(rowp);
+        acc[0] += bf16_scaled(w4.x << 16);
+        acc[1] += bf16_scaled(w4.x);   // (the low half is masked off by the encoding)
+        acc[2] += bf16_scaled(w4.y << 16);
+        acc[3] += bf16_scaled(w4.y);
+        acc[4] += bf16_scaled(w4.z << 16);
+        acc[5] += bf16_scaled(w4.z);
+        acc[6] += bf16_scaled(w4.w << 16);
+        acc[7] += bf16_scaled(w4.w);
+        const uint32_t m0 = w4.x & 0x7FFF7FFFu, m1 = w4.y & 0x7FFF7FFFu, m2 = w4.z & 0x7FFF7FFFu,
+                       m3 = w4.w & 0x7FFF7FFFu;
+        pmax = __vimax3_u16x2(pmax, __vimax3_u16x2(m0, m1, m2), m3);
+        pmin = __vimin3_u16x2(pmin, __vimin3_u16x2(m0, m1, m2), m3);
+      }
+      const bool zero_here = (pmin & 0xFFFFu) == 0 || (pmin >> 16) == 0;
+      if (text_k || zero_here) {
+        // text keys also go to k_cat raw (fp64; 2 blocks per head); an exact
+        // zero: this part's minimum over NONZERO magnitudes (0 -> 0x7FFF key)
+        double* raw_out =
+            text_k ? ws.k_cat + ((int64_t)it.h * g.n_cols + n_q + (kv_row0(g, it.blk) - g.Tv) + r0) * D : nullptr;
+        uint32_t kmin = 0x7FFF7FFFu;
+        for (int r = rl; r < rows; r += RPI) {
+          const uint4 w4 = *reinterpret_cast<const uint4*>(stage + r * D * 2 + tc * 16);
+          const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          raw_out[r * D + tc * 8 + 2 * j] = (double)__uint_as_float(w[j] << 16);
-          raw_out[r * D + tc * 8 + 2 * j + 1] = (double)__uint_as_float(w[j] & 0xFFFF0000u);
+          for (int j = 0; j < 4; ++j) {
+            kmin = __vminu2(kmin, ((w[j] & 0x7FFF7FFFu) + 0x7FFF7FFFu) & 0x7FFF7FFFu);
+            if (raw_out) {
+              raw_out[r * D + tc * 8 + 2 * j] = (double)__uint_as_float(w[j] << 16);
+              raw_out[r * D + tc * 8 + 2 * j + 1] = (double)__uint_as_float(w[j] & 0xFFFF0000u);
+            }
+          }
+        }
+        if (zero_here) {
+          // this part's nonzero minimum: key + 1 (a 0x7FFF key: only zeros -> 0xFFFF, none)
+          const uint32_t k0 = kmin & 0xFFFFu, k1 = kmin >> 16;
+          const uint32_t n0 = k0 == 0x7FFFu ? 0xFFFFu : k0 + 1, n1 = k1 == 0x7FFFu ? 0xFFFFu : k1 + 1;
+          pmin = (n1 << 16) | n0;
         }
       }
+      nzmin = __vminu2(nzmin, pmin);
+      if (kp && (it.seg > 0 || qp) && lane == 0 && rows > 0)
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // permuted copy read out
+      __syncwarp();
+      // stage st is consumed: refill it with the load NST ahead
+      if (!perm && lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(st);
+      if (perm) asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    uint32_t tmax = max(pmax & 0xFFFFu, pmax >> 16);
-    uint32_t tmin = min(pmin & 0xFFFFu, pmin >> 16);
-    if (tmin == 0) {
-      // an exact zero: the minimum over NONZERO magnitudes (0 -> 0x7FFF key)
-      uint32_t kmin = 0x7FFF7FFFu;
-      for (int64_t r = rp; r < len; r += RP) {
-        const uint4 w4 = *reinterpret_cast<const uint4*>(blk + r * D * 2 + tc * 16);
-        const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) kmin = __vminu2(kmin, ((w[j] & 0x7FFF7FFFu) + 0x7FFF7FFFu) & 0x7FFF7FFFu);
-      }
-      const uint32_t km = min(kmin & 0xFFFFu, kmin >> 16);
-      tmin = km == 0x7FFFu ? 0xFFFFu : km + 1;   // 0xFFFF: no nonzero value
-    }
-    // lanes holding the same 8 columns (other row phases) merge their sums
+    // ---- this item's column sums, exactness, outputs (all in the warp) ----
 #pragma unroll
     for (int o = TPR; o < 32; o <<= 1)
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      tmax = max(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
-      tmin = min(tmin, __shfl_xor_sync(0xffffffffu, tmin, o));
-    }
-    if (lane < TPR) {
-      double2* dst = reinterpret_cast<double2*>(s_part + (buf * WARPS + warp) * D + tc * 8);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) dst[j] = make_double2(acc[2 * j], acc[2 * j + 1]);
-    }
-    if (lane == 0) {
-      s_rng[(buf * WARPS + warp) * 2] = tmax;
-      s_rng[(buf * WARPS + warp) * 2 + 1] = tmin;
-    }
-    if (t == 0 && kp) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // permuted copy read out
-    __syncthreads();
-    // ---- decision (uniform) ----
-    uint32_t mx = 0, mn = 0xFFFFu;
-#pragma unroll
-    for (int w2 = 0; w2 < WARPS; ++w2) {
-      mx = max(mx, s_rng[(buf * WARPS + w2) * 2]);
-      mn = min(mn, s_rng[(buf * WARPS + w2) * 2 + 1]);
-    }
-    if (t == 0 && mx >= 0x7F80u) atomicOr(ws.status + ST_NONFINITE, 1);   // exponent field 0xFF: inf / NaN
-    const int lg = len > 1 ? 32 - __clz((int)(len - 1)) : 0;
+    uint32_t tmax = max(pmax & 0xFFFFu, pmax >> 16);
+    uint32_t tmin = min(nzmin & 0xFFFFu, nzmin >> 16);
+    tmax = __reduce_max_sync(0xffffffffu, tmax);
+    tmin = __reduce_min_sync(0xffffffffu, tmin);
+    if (lane == 0 && tmax >= 0x7F80u) atomicOr(ws.status + ST_NONFINITE, 1);   // exponent 0xFF: inf / NaN
+    const int lg = len > 1 ? 32 - __clz(len - 1) : 0;
     // exponent fields (bits >> 7); subnormals (field 0) count as exponent 1
-    const int emax = max(1, (int)(mx >> 7)), emin = max(1, (int)(mn >> 7));
-    const bool exact = (mn == 0xFFFFu) || (emax - emin + 8 + lg < 53);
-    double sum = 0.0;
-    if (!exact) {
-      if (t < D)
-        sum = fsum_exact(len, [&](int64_t r) {
-          return (double)__bfloat162float(reinterpret_cast<const __nv_bfloat16*>(blk)[r * D + t]);
-        });
-      __syncthreads();   // every column has been read from the stage
+    const int emax = max(1, (int)(tmax >> 7)), emin = max(1, (int)(tmin >> 7));
+    const bool exact = (tmin >= 0xFFFFu) || (emax - emin + 8 + lg < 53);
+    const bool pow2 = (len & (len - 1)) == 0;
+    const int64_t h = it.h;
+    double* dst_mean;
+    double* dst_def = nullptr;
+    if (it.seg == 0) {
+      dst_mean = ws.q_pool + (h * g.N + it.blk) * D;
+      dst_def = ws.q_def + (h * g.N + it.blk) * D;
+    } else if (it.seg == 1) {
+      const int64_t kc_row = it.blk < n_q ? it.blk : g.N + g.Tt + (it.blk - n_q);
+      dst_mean = ws.k_cat + (h * g.n_cols + kc_row) * D;
+      dst_def = ws.k_def + (h * g.M + it.blk) * D;
+    } else {
+      dst_mean = ws.v_pool + (h * g.M + it.blk) * D;
     }
-    // ---- refill stage st with this CTA's item STAGES ahead ----
-    {
-      const int64_t nx = i + (int64_t)STAGES * gridDim.x;
-      if (perm) {
-        if (nx < n_items) fetch_rows(nx, st);
-        asm volatile("cp.async.commit_group;" ::: "memory");
-      } else if (t == 0 && nx < n_items) {
-        fetch(nx, st);
-      }
-    }
-    // ---- phase B ----
-    if (t < D) {
-      const int col = t;
-      if (exact) {
-#pragma unroll
-        for (int w2 = 0; w2 < WARPS; ++w2) sum += s_part[(buf * WARPS + w2) * D + col];
-        sum = unscale_896(sum);
-      }
-      const double flen = (double)len;
-      const double mean = sum / flen;            // core.py:172 fsum(...) / length
+    bool nonzero_def = false;
+    auto finish = [&](int col, double sum) {
+      // core.py:172 fsum(...) / length; a power-of-two length divides exactly
+      // by its reciprocal (and then the deficit is exactly 0)
+      const double mean = pow2 ? __dmul_rn(sum, 1.0 / (double)len) : sum / (double)len;
       // numpy rounds the product first (no FMA contraction): masks.py:166 / masks.py:171
-      const double deficit = __dsub_rn(sum, __dmul_rn(flen, mean));
-      if (it.seg == 0) {
-        ws.q_pool[(it.h * g.N + it.blk) * D + col] = mean;
-        ws.q_def[(it.h * g.N + it.blk) * D + col] = deficit;
-      } else if (it.seg == 1) {
-        const int64_t kc_row = it.blk < g.N ? it.blk : g.N + g.Tt + (it.blk - g.N);
-        ws.k_cat[(it.h * g.n_cols + kc_row) * D + col] = mean;
-        ws.k_def[(it.h * g.M + it.blk) * D + col] = deficit;
-      } else {
-        ws.v_pool[(it.h * g.M + it.blk) * D + col] = mean;
+      const double deficit = pow2 ? 0.0 : __dsub_rn(sum, __dmul_rn((double)len, mean));
+      dst_mean[col] = mean;
+      if (dst_def) dst_def[col] = deficit;
+      nonzero_def |= deficit != 0.0;
+    };
+    if (exact) {
+      if (lane < TPR) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) finish(tc * 8 + j, unscale_896(acc[j]));
       }
-      if (it.seg < 2 && deficit != 0.0) atomicOr(ws.status + ST_DEFICIT, 1);
+    } else {
+      // correctly rounded column sums (math.fsum), re-read from global memory
+      const __nv_bfloat16* src = bases[it.seg];
+      for (int col = lane; col < D; col += 32) {
+        const double sum = fsum_exact(len, [&](int64_t r) {
+          const int64_t row = (perm && it.blk < n_q) ? perm[(int64_t)it.blk * B + r] : kv_row0(g, it.blk) + r;
+          return (double)__bfloat162float(src[row_off(g, it.h, row) + col]);
+        });
+        finish(col, sum);
+      }
     }
+    if (it.seg < 2 && __any_sync(0xffffffffu, nonzero_def) && lane == 0) atomicOr(ws.status + ST_DEFICIT, 1);
   }
-  if (t == 0 && kp) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (lane == 0 && kp) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 template <int D>
 cudaError_t launch_bulk(const Geometry& g, const void* q, const void* k, const void* v, const Workspace& ws,
                         cudaStream_t st, const int32_t* perm, void* kp, void* vp, void* qp) {
-  constexpr int STAGES = 3;
-  constexpr int WARPS = kBulkThreads / 32;
-  const size_t smem = (size_t)STAGES * g.B * D * 2 + STAGES * 8 + 2 * WARPS * D * 8 + 2 * WARPS * 2 * 4;
+  const int stage_rows = (int)std::min<int64_t>(g.B, RSA_K1_PART_BYTES / (D * 2));
+  const size_t smem = (size_t)RSA_K1_STAGES * stage_rows * D * 2 + RSA_K1_STAGES * 8;
+  if (g.H * (g.N + 2 * g.M) >= ((int64_t)1 << 31)) return cudaErrorNotSupported;
   CUtensorMap tq, tk, tv;
-  if (!make_rows_tmap(&tq, q, g, D, (int)g.B, CU_TENSOR_MAP_SWIZZLE_NONE) ||
-      !make_rows_tmap(&tk, k, g, D, (int)g.B, CU_TENSOR_MAP_SWIZZLE_NONE) ||
-      !make_rows_tmap(&tv, v, g, D, (int)g.B, CU_TENSOR_MAP_SWIZZLE_NONE))
+  if (!make_rows_tmap(&tq, q, g, D, stage_rows, CU_TENSOR_MAP_SWIZZLE_NONE) ||
+      !make_rows_tmap(&tk, k, g, D, stage_rows, CU_TENSOR_MAP_SWIZZLE_NONE) ||
+      !make_rows_tmap(&tv, v, g, D, stage_rows, CU_TENSOR_MAP_SWIZZLE_NONE))
     return cudaErrorInvalidValue;
-  auto kern = pool_bulk_kernel<D, STAGES>;
+  auto kern = pool_warp_kernel<D>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t n_items = g.H * (g.N + 2 * g.M);
-  const int64_t grid = std::min<int64_t>(n_items, (int64_t)sms * 2);
-  kern<<<(unsigned)grid, kBulkThreads, smem, st>>>(tq, tk, tv, (const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
-                                                   (const __nv_bfloat16*)v, ws, g, n_items, perm,
-                                                   (__nv_bfloat16*)kp, (__nv_bfloat16*)vp, (__nv_bfloat16*)qp);
+  const int n_items = (int)(g.H * (g.N + 2 * g.M));
+  const int grid = (int)std::min<int64_t>(n_items, (int64_t)sms * RSA_K1_CTAS_PER_SM);
+  kern<<<(unsigned)grid, 32, smem, st>>>(tq, tk, tv, (const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
+                                          (const __nv_bfloat16*)v, ws, g, n_items, stage_rows, perm,
+                                          (__nv_bfloat16*)kp, (__nv_bfloat16*)vp, (__nv_bfloat16*)qp);
   return cudaGetLastError();
 }
 
@@ -552,7 +560,7 @@ cudaError_t launch_pool(const Geometry& g, const void* q, const void* k, const v
       // that fits two ring stages per CTA, three CTAs per SM
       const bool aligned = ((uintptr_t)q % 16 == 0) && ((uintptr_t)k % 16 == 0) && ((uintptr_t)v % 16 == 0);
       // rows 16-byte aligned for TMA; three ring stages + partials fit two CTAs per SM
-      const bool fits = g.B * g.d * 2 * 3 <= 96 * 1024 && g.B <= 256 && (g.s_tok * 2) % 16 == 0 &&
+      const bool fits = g.B * g.d * 2 <= 32 * 1024 && g.B <= 256 && (g.s_tok * 2) % 16 == 0 &&
                         (g.s_head * 2) % 16 == 0 && (g.s_batch * 2) % 16 == 0;
       if (aligned && fits && g.d == 128) return launch_bulk<128>(g, q, k, v, ws, st, perm, kp, vp, qp);
       if (aligned && fits && g.d == 64) return launch_bulk<64>(g, q, k, v, ws, st, perm, kp, vp, qp);

@@ -439,6 +439,36 @@ def test_bf16_pooling_bit_exact(scale_range, d, block):
     np.testing.assert_array_equal(res.pooled.k_mix_pool.cpu().numpy(), ref["k_mix"])
 
 
+@pytest.mark.parametrize("d,block,t_t", [(64, 64, 100), (128, 128, 131)])
+def test_bf16_pooling_bit_exact_hard_cases(d, block, t_t):
+    """K1 against math.fsum on blocks built to break naive summation: exact
+    zeros (the nonzero-minimum path), bf16 subnormals, 2^+-40 and 2^-120 magnitudes in
+    one column with exact cancellations (the Shewchuk fallback must round
+    correctly, where a (hi, lo) TwoSum merge need not), rows that are all zero,
+    and a ragged text block (len 3 at d 128, B 128: non-power-of-two mean and
+    deficit, compared bitwise through q_def / k_def via the GAPR error)."""
+    rng = np.random.default_rng(23)
+    t_v = block * 12
+    qv, qt, k, v = (O.round_to_bf16(x) for x in O.random_problem(4, t_v=t_v, t_t=t_t, d=d, dtype=np.float32))
+    big = np.float32(2.0 ** 40)
+    for x in (qv, k, v):
+        x[rng.random(x.shape) < 0.2] = 0.0                                  # exact zeros
+        x[block:2 * block] = 0.0                                            # an all-zero block
+        x[2 * block:2 * block + 5, :] *= np.float32(2.0 ** -120)            # subnormal bf16 values
+        x[3 * block, :] = big                                               # big + ... - big:
+        x[3 * block + 1, :] = -big                                          # cancels exactly
+        x[3 * block + 2, :] = O.round_to_bf16(np.float32(3.0) * np.float32(2.0 ** -60))
+        x[4 * block:4 * block + 3, :] = O.round_to_bf16(rng.standard_normal((3, d)).astype(np.float32) * big)
+    qv, qt, k, v = (O.round_to_bf16(x) for x in (qv, qt, k, v))
+    res = rsa.rectified_attention_pipeline(bf16_problem(qv, qt, k, v, block), SparsityConfig(0.2, 0.0, 0, False))
+    ref = O.pool(qv, k, v, t_t, block)
+    np.testing.assert_array_equal(res.pooled.q_pool.cpu().numpy(), ref["q_pool"])
+    np.testing.assert_array_equal(res.pooled.v_pool.cpu().numpy(), ref["v_pool"])
+    np.testing.assert_array_equal(res.pooled.k_mix_pool.cpu().numpy(), ref["k_mix"])
+    np.testing.assert_array_equal(res.comp_mask.mask.cpu().numpy(),
+                                  O.pipeline(qv, qt, k, v, block, 0.2, 0.0, 0, False)["comp"])
+
+
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32, torch.float64])
 @pytest.mark.parametrize("where", ["q_video", "k", "v"])
 def test_non_finite_inputs_raise_shape_error(dtype, where):

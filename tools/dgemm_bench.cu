@@ -41,8 +41,8 @@ int main() {
         cublasDgemmStridedBatched(hb, CUBLAS_OP_N, CUBLAS_OP_N, c.N, c.M, c.K, &one, B, c.N, sb, A, c.K, sa, &zero,
                                   C2, c.N, sc, H);
     };
-    for (cfg = 1; cfg <= 5; ++cfg) {
-    if (cfg == 5) cfg = 0;
+    for (cfg = 1; cfg <= 9; ++cfg) {
+    if (cfg == 9) cfg = 0;
     for (int w = 0; w < 3; ++w) { ours(); theirs(); }
     float t_o = 0, t_c = 0;
     const int R = 20;
