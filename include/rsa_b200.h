@@ -48,20 +48,18 @@ typedef enum {
   RSA_VARIANT_COMPENSATE_ALL = 4
 } rsa_variant;
 
-/* Attention kernel selection (K3). AUTO picks the tcgen05 kernels for bf16 and
- * block/head_dim in {64,128} (the two-tile ping-pong kernel at block = head_dim
- * = 128, the persistent one-tile kernel otherwise), the CUDA-core kernel for
- * everything else (fp32/fp64, other block sizes). */
-/* AUTO: bf16 -> the tcgen05 kernel of the shape class (d = B = 128: the
- * two-tile ping-pong kernel; else the one-tile persistent kernel), f32/f64 ->
- * the CUDA-core kernel.  TCGEN05_PERSISTENT forces the one-tile persistent
- * tcgen05 kernel at d = B = 128 and SIMT the CUDA-core kernel for bf16
- * (cross-checks; never chosen silently). */
+/* Attention kernel selection (K3).  AUTO / TCGEN05: bf16 -> the tcgen05 kernel
+ * of the shape class (d = B = 128: the paired-tile kernel; block or head_dim 64:
+ * the one-tile persistent kernel), f32/f64 -> the CUDA-core kernel.
+ * TCGEN05_PERSISTENT / TCGEN05_PINGPONG force the one-tile persistent or the
+ * two-slot ping-pong tcgen05 kernel at d = B = 128, and SIMT the CUDA-core
+ * kernel for bf16 (cross-checks; never chosen silently). */
 typedef enum {
   RSA_KERNEL_AUTO = 0,
   RSA_KERNEL_TCGEN05 = 1,
   RSA_KERNEL_SIMT = 2,
-  RSA_KERNEL_TCGEN05_PERSISTENT = 3
+  RSA_KERNEL_TCGEN05_PERSISTENT = 3,
+  RSA_KERNEL_TCGEN05_PINGPONG = 4
 } rsa_kernel;
 
 /* rsa_shape.flags */

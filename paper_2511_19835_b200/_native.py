@@ -18,7 +18,7 @@ LIB_PATH = Path(os.environ.get("RSA_B200_LIB", Path(__file__).resolve().parent /
 DTYPE_CODES = {"bfloat16": 0, "float32": 1, "float64": 2}
 VARIANT_CODES = {"full": 0, "sparse-unrectified": 1, "sparse-rectified": 2,
                  "sparse-rectified-no-gapr": 3, "compensate-all": 4}
-KERNEL_CODES = {"auto": 0, "tcgen05": 1, "simt": 2, "tcgen05-persistent": 3}
+KERNEL_CODES = {"auto": 0, "tcgen05": 1, "simt": 2, "tcgen05-persistent": 3, "tcgen05-pingpong": 4}
 
 EXPORTS = ("rsa_plan", "rsa_workspace_layout_query", "rsa_workspace_size", "rsa_pool",
            "rsa_select", "rsa_attention", "rsa_forward", "rsa_forward_host", "rsa_block_sparse_attention",

@@ -960,6 +960,609 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
   }
 }
 
+// ============================================================================
+// Paired-tile kernel (d = B = 128, the default): two 128-row query tiles per
+// CTA, each walking its own kv list, and ONE MMA-issuing thread interleaving
+// them in the order  S0_j, PV1_{j-1}, S1_j, PV0_j  (FA4-style), so each tile's
+// softmax runs while the tensor pipe executes the other tile's two MMA groups,
+// and every S is a full 128-key MMA group (no 64-key sub-steps: half the
+// barrier round trips per FLOP of the ping-pong kernel, and the SS operand
+// traffic stays at the shared-memory rate).
+//   TMEM   S0 | S1 | O0 | O1 (4 x 128 fp32 columns); P_t is written as bf16
+//          pairs over the first 64 columns of S_t (the TS-MMA A operand).
+//   smem   Q0, Q1 (32 KB each) + a 5-stage ring of 32 KB K / V blocks,
+//          filled in exactly the MMA consumption order.
+//   warps  0 TMA producer (K/V ring), 1 MMA issuer (+ TMEM owner), 2-3 K/V
+//          readiness checkers of tiles 0/1 (warpgroup 0 runs on 80 registers), 4-7 softmax +
+//          epilogue of tile 0, 8-11 of tile 1 (one thread per row, 208
+//          registers: all 128 scores of a row stay in registers).  The
+//          setmaxnreg budgets move registers inside the CTA's own pool
+//          (384 x 168 at launch): 128 x (168 - 80) >= 256 x (208 - 168).
+// Ordering facts the pipeline relies on (no extra barriers):
+//   * the tensor pipe executes one thread's MMAs in issue order, so S_t_{j+1}
+//     (issued after PV_t_j) cannot overwrite P_t_j before PV_t_j read it;
+//   * tcgen05.commit tracks every earlier MMA of the issuing thread, so the
+//     s_full[t] phase of block j implies PV_t_{j-1} is complete: the softmax
+//     may rescale O_t right there;
+//   * a softmax group finishes its epilogue (reads of O_t) before it releases
+//     P_t of its next tile, and the next tile's first PV_t waits on that P_t.
+// Q_t of a slot's next tile is TMA-loaded by the slot's own softmax group as
+// soon as the last S_t of the current tile has completed (Q_t is then free).
+// ============================================================================
+// tools-only timeline of CTA 0 (-DRSA_PAIR_TRACE; tools/pair_trace.py): region 0 the
+// MMA thread (per MMA group: clock before its waits, after the P wait, after
+// the K/V wait), regions 1-2 row 0 of each softmax group (per block: before the
+// S wait, after it, after the P release), region 3 the producer (per K/V load:
+// clock before the ring-slot wait, at the TMA issue)
+#ifdef RSA_PAIR_TRACE
+__device__ long long g_pair_trace[4][16384];
+#define PAIR_TRACE(region, idx, v) \
+  do { if (blockIdx.x == 0 && (idx) < 16384) g_pair_trace[region][idx] = (v); } while (0)
+#else
+#define PAIR_TRACE(region, idx, v) do {} while (0)
+#endif
+
+struct CfgPair {
+  static constexpr int D = 128, BKV = 128;
+  static constexpr int NST = 5;                    // K/V ring stages
+  static constexpr int STAGE = BKV * D * 2;        // 32 KB
+  static constexpr int PANEL = 128 * 128;          // 16 KB: 128 rows x 128 B (64 columns)
+  static constexpr int Q_BYTES = 128 * D * 2;      // 32 KB
+  static constexpr int HEAD = 256 + 2 * 128 * 4;   // barriers + tmem slot | parked compensation rows [2][128]
+  static constexpr int SMEM = HEAD + 1024 + 2 * Q_BYTES + NST * STAGE;   // 231,680 <= 232,448
+  static constexpr uint32_t IDESC_S = ptx::idesc_bf16(128, 128, false);
+  static constexpr uint32_t IDESC_O = ptx::idesc_bf16(128, D, true);   // V MN-major
+  static constexpr int THREADS = 384;
+};
+#ifndef RSA_PAIR_POLY
+#define RSA_PAIR_POLY 0   // column pairs per 32-column chunk whose 2^x runs on the FMA pipe
+#endif
+#ifndef RSA_PAIR_L2PF
+#define RSA_PAIR_L2PF 0   // iterations ahead whose K/V blocks the producer prefetches into L2 (0: off)
+#endif
+
+__global__ void __launch_bounds__(384, 1)
+attn_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                    const __grid_constant__ CUtensorMap tm_v, const TcParams P, int64_t n_tiles) {
+  using C = CfgPair;
+  constexpr int D = C::D;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* q_full = bars;            // [2] tx: the slot's Q tile landed
+  uint64_t* s_full = bars + 2;        // [2] commit: S_t complete (and every earlier MMA)
+  uint64_t* p_full = bars + 4;        // [2] 129 arrivals: P_t written (O_t rescaled if needed), V_t_j and
+                                      //     K_t_{j+1} landed
+  uint64_t* o_full = bars + 6;        // [2] commit: the tile's last PV_t complete
+  uint64_t* kv_full = bars + 8;       // [NST]
+  uint64_t* kv_empty = bars + 8 + C::NST;   // [NST]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8 + 2 * C::NST);
+  float* comp_s = reinterpret_cast<float*>(smem_raw + 256);   // [slot][128] this tile's compensation row
+  uint8_t* data = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw + C::HEAD) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* q_s = data;                       // [2][Q_BYTES]
+  uint8_t* ring = data + 2 * C::Q_BYTES;     // [NST][STAGE]
+
+  const Geometry& g = P.g;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t n_pairs = (n_tiles + 1) / 2;
+  if (threadIdx.x == 0) {
+    for (int t = 0; t < 2; ++t) {
+      ptx::mbar_init(q_full + t, 1);
+      ptx::mbar_init(s_full + t, 1);
+      ptx::mbar_init(p_full + t, 129);   // the group's 128 rows + the K/V readiness checker
+      ptx::mbar_init(o_full + t, 1);
+    }
+    for (int i = 0; i < C::NST; ++i) {
+      ptx::mbar_init(kv_full + i, 1);
+      ptx::mbar_init(kv_empty + i, 1);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) {
+    ptx::regs_dec<80>();
+    if (warp == 0 && lane == 0) {
+    // ===================== TMA producer: K/V blocks in MMA order =====================
+      ptx::prefetch_tmap(&tm_k);
+      ptx::prefetch_tmap(&tm_v);
+      const uint64_t keep = ptx::policy_evict_last();   // K/V blocks are re-read by many tiles of the head
+      int st = 0;
+      uint32_t ph = 0;
+      int ptr = 0;   // trace index (RSA_PAIR_TRACE)
+      (void)ptr;
+      for (int64_t pr = blockIdx.x; pr < n_pairs; pr += gridDim.x) {
+        const int64_t b1 = 2 * pr + 1;
+        const TileDesc t0 = decode_tile(P, 2 * pr);
+        const TileDesc t1 = b1 < n_tiles ? decode_tile(P, b1) : TileDesc{};
+        const int c0 = (int)t0.count;
+        const int c1 = b1 < n_tiles ? (int)t1.count : 0;
+        const int h0 = (int)t0.h, h1 = (int)t1.h, f0 = (int)t0.m_first, f1 = (int)t1.m_first;
+        const int32_t* l0 = t0.list;
+        const int32_t* l1 = t1.list;
+        const int cmax = c0 > c1 ? c0 : c1;
+        // kv-list entries are read one iteration ahead: a dependent global load
+        // between the kv_empty wait and the TMA issue would sit on the ring's
+        // refill path (it did: ~300-cycle S waits)
+        auto kv_of = [&](const int32_t* lst, int f, int jj) { return lst ? (__ldg(lst + jj) & 0xFFFFFF) : f + jj; };
+        int m0 = c0 > 0 ? kv_of(l0, f0, 0) : 0, m1 = c1 > 0 ? kv_of(l1, f1, 0) : 0, m1_prev = 0;
+        int pf0 = 0, pf1 = 0;   // (RSA_PAIR_L2PF) kv blocks of iteration j + RSA_PAIR_L2PF
+        if (RSA_PAIR_L2PF > 0) {
+          pf0 = RSA_PAIR_L2PF < c0 ? kv_of(l0, f0, RSA_PAIR_L2PF) : 0;
+          pf1 = RSA_PAIR_L2PF < c1 ? kv_of(l1, f1, RSA_PAIR_L2PF) : 0;
+        }
+        (void)pf0; (void)pf1;
+        for (int j = 0; j <= cmax; ++j) {
+          const int n0 = j + 1 < c0 ? kv_of(l0, f0, j + 1) : 0;
+          const int n1 = j + 1 < c1 ? kv_of(l1, f1, j + 1) : 0;
+          if (RSA_PAIR_L2PF > 0) {
+            const int jp = j + RSA_PAIR_L2PF;
+            const int q0 = jp + 1 < c0 ? kv_of(l0, f0, jp + 1) : 0;
+            const int q1 = jp + 1 < c1 ? kv_of(l1, f1, jp + 1) : 0;
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+              if (jp < c0) {
+                ptx::tma_prefetch_3d(&tm_k, 64 * p, (int)kv_row0(g, pf0), h0);
+                ptx::tma_prefetch_3d(&tm_v, 64 * p, (int)kv_row0(g, pf0), h0);
+              }
+              if (jp < c1) {
+                ptx::tma_prefetch_3d(&tm_k, 64 * p, (int)kv_row0(g, pf1), h1);
+                ptx::tma_prefetch_3d(&tm_v, 64 * p, (int)kv_row0(g, pf1), h1);
+              }
+            }
+            pf0 = q0;
+            pf1 = q1;
+          }
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            // MMA order: K0_j, V1_{j-1}, K1_j, V0_j
+            const int tt = (q4 == 0 || q4 == 3) ? 0 : 1;
+            const int jj = q4 == 1 ? j - 1 : j;
+            const int cc = tt ? c1 : c0;
+            if (jj < 0 || jj >= cc) continue;
+            const int m = q4 == 1 ? m1_prev : (tt ? m1 : m0);
+            PAIR_TRACE(3, ptr, clock64());
+            ptx::mbar_wait(kv_empty + st, ph ^ 1);
+            PAIR_TRACE(3, ptr + 1, clock64());
+            ptr += 2;
+            ptx::mbar_expect_tx(kv_full + st, C::STAGE);
+            uint8_t* dst = ring + st * C::STAGE;
+            const CUtensorMap* tmap = (q4 & 1) ? &tm_v : &tm_k;
+            const int row0 = (int)kv_row0(g, m), hh = tt ? h1 : h0;
+#pragma unroll
+            for (int p = 0; p < 2; ++p)
+              ptx::tma_load_3d_hint(dst + p * C::PANEL, tmap, kv_full + st, 64 * p, row0, hh, keep);
+            if (++st == C::NST) { st = 0; ph ^= 1; }
+          }
+          m1_prev = m1;
+          m0 = n0;
+          m1 = n1;
+        }
+      }
+    } else if (warp == 1) {
+    // ===================== MMA issuer: S0_j, PV1_{j-1}, S1_j, PV0_j =====================
+    // In steady state the only waits are the two p_full phases per iteration:
+    // p_full[t] of block j also certifies (checker warp 2 + t) that V_t_j and
+    // K_t_{j+1} have landed, so each wait releases a PV group and the next S
+    // group of the same tile back to back.  A wait on an mbarrier costs the
+    // issuing thread ~250 cycles behind its queued MMAs, during which the
+    // tensor pipe ran dry with one wait per group.
+    const uint32_t q_addr = ptx::smem_u32(q_s);
+    const uint32_t ring_addr = ptx::smem_u32(ring);
+    int st = 0;
+    uint32_t ph = 0;
+    uint32_t pbits = 0, qbits = 0;   // p_full / q_full parity per slot (bit t)
+    int tr = 0;   // trace index (RSA_PAIR_TRACE)
+    (void)tr;
+    auto issue_s = [&](int t, bool first_of_tile) {
+      PAIR_TRACE(0, tr, (clock64() << 2) | (t ? 2 : 0));
+      PAIR_TRACE(0, tr + 1, 0);
+      if (first_of_tile) {   // Q_t and K_t_0 are nobody else's to certify
+        ptx::mbar_wait(q_full + t, (qbits >> t) & 1u);
+        qbits ^= 1u << t;
+        ptx::mbar_wait(kv_full + st, ph);
+        ptx::tc_fence_after();
+      }
+      PAIR_TRACE(0, tr + 2, clock64());
+      tr += 3;
+      const uint32_t kb = ring_addr + (uint32_t)(st * C::STAGE);
+      const uint32_t qb = q_addr + (uint32_t)(t * C::Q_BYTES);
+      if (ptx::elect_one()) {
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (uint32_t)((k / 4) * C::PANEL + (k % 4) * 32);
+          ptx::mma_ss(tmem + (uint32_t)(t * 128), ptx::sw128_desc(qb + off, 16, 1024),
+                      ptx::sw128_desc(kb + off, 16, 1024), C::IDESC_S, k > 0);
+        }
+        ptx::tc_commit(kv_empty + st);   // K block read
+        ptx::tc_commit(s_full + t);
+      }
+      __syncwarp();
+      if (++st == C::NST) { st = 0; ph ^= 1u; }
+    };
+    auto issue_pv = [&](int t, bool first, bool last) {
+      PAIR_TRACE(0, tr, (clock64() << 2) | (t ? 1 : 3));
+      ptx::mbar_wait(p_full + t, (pbits >> t) & 1u);   // P_t_j written, V_t_j (and K_t_{j+1}) landed
+      pbits ^= 1u << t;
+      ptx::tc_fence_after();
+      PAIR_TRACE(0, tr + 1, clock64());
+      PAIR_TRACE(0, tr + 2, clock64());
+      tr += 3;
+      const uint32_t vb = ring_addr + (uint32_t)(st * C::STAGE);
+      if (ptx::elect_one()) {
+#pragma unroll
+        for (int k = 0; k < 128 / 16; ++k)
+          ptx::mma_ts(tmem + 256u + (uint32_t)(t * 128), tmem + (uint32_t)(t * 128) + k * 8,
+                      ptx::sw128_desc(vb + k * 2048, C::PANEL, 1024), C::IDESC_O, (!first || k > 0) ? 1u : 0u);
+        ptx::tc_commit(kv_empty + st);   // V block read
+        if (last) ptx::tc_commit(o_full + t);
+      }
+      __syncwarp();
+      if (++st == C::NST) { st = 0; ph ^= 1u; }
+    };
+    for (int64_t pr = blockIdx.x; pr < n_pairs; pr += gridDim.x) {
+      const int64_t b1 = 2 * pr + 1;
+      const bool e1 = b1 < n_tiles;
+      const int c0 = (int)decode_tile(P, 2 * pr).count;
+      const int c1 = e1 ? (int)decode_tile(P, b1).count : 0;
+      const int cmax = c0 > c1 ? c0 : c1;
+      if (c0 > 0) issue_s(0, true);
+      for (int j = 0; j <= cmax; ++j) {
+        if (j >= 1 && j <= c1) issue_pv(1, j == 1, j == c1);
+        if (j < c1) issue_s(1, j == 0);
+        if (j < c0) {
+          issue_pv(0, j == 0, j == c0 - 1);
+          if (j + 1 < c0) issue_s(0, false);
+        }
+      }
+      // a tile with an empty kv list (the C ABI's mask seam flags it as
+      // RSA_ERR_EMPTY_ROW): its group still loaded Q and releases one P phase
+      // after its previous epilogue; answer with the o_full phase (so o_full
+      // can never run a phase ahead of the group)
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        if ((t == 0 ? c0 : c1) == 0 && (t == 0 || e1)) {
+          ptx::mbar_wait(q_full + t, (qbits >> t) & 1u);
+          qbits ^= 1u << t;
+          ptx::mbar_wait(p_full + t, (pbits >> t) & 1u);
+          pbits ^= 1u << t;
+          if (ptx::elect_one()) ptx::tc_commit(o_full + t);
+          __syncwarp();
+        }
+      }
+    }
+    } else if (lane == 0) {
+    // ===================== K/V readiness checker of slot t = warp - 2 =====================
+    // Adds its own arrival to p_full[t] of block j once V_t_j and K_t_{j+1}
+    // have landed (the ring position of every load is a function of the pair's
+    // two counts), then waits for that phase so it never arrives a phase early.
+    const int t = warp - 2;
+    uint32_t base = 0, pph = 0;
+    for (int64_t pr = blockIdx.x; pr < n_pairs; pr += gridDim.x) {
+      const int64_t b1 = 2 * pr + 1;
+      const bool e1 = b1 < n_tiles;
+      const int c0 = (int)decode_tile(P, 2 * pr).count;
+      const int c1 = e1 ? (int)decode_tile(P, b1).count : 0;
+      if (t == 0 || e1) {
+        // items in iterations [0, j): K0, V1_{i-1}, K1, V0 per iteration i
+        auto cnt = [&](int j) { return 2 * min(j, c0) + min(j, c1) + max(0, min(j - 1, c1)); };
+        auto wait_item = [&](uint32_t pos) {
+          ptx::mbar_wait(kv_full + (pos % C::NST), (pos / C::NST) & 1u);
+        };
+        const int ct = t ? c1 : c0;
+        for (int j = 0; j < ct; ++j) {
+          uint32_t pv, pk;
+          if (t == 0) {
+            pv = base + cnt(j) + 1 + (j >= 1 && j <= c1) + (j < c1);        // V0_j
+            pk = base + cnt(j + 1);                                          // K0_{j+1}
+          } else {
+            pv = base + cnt(j + 1) + (j + 1 < c0);                           // V1_j
+            pk = base + cnt(j + 1) + (j + 1 < c0) + (j + 1 <= c1);           // K1_{j+1}
+          }
+          wait_item(pv);
+          if (j + 1 < ct) wait_item(pk);
+          ptx::mbar_arrive(p_full + t);
+          ptx::mbar_wait(p_full + t, pph);
+          pph ^= 1u;
+        }
+        if (ct == 0) {   // the empty tile's single P phase
+          ptx::mbar_arrive(p_full + t);
+          ptx::mbar_wait(p_full + t, pph);
+          pph ^= 1u;
+        }
+      }
+      base += 2u * (uint32_t)(c0 + c1);
+    }
+    }
+  } else {
+    ptx::regs_inc<208>();
+    // ===================== softmax + epilogue of slot t, one thread per row =====================
+    const int t = (warp - 4) >> 2;
+    const int quad = warp & 3;                 // TMEM lane quadrant this warp may access
+    const int row = quad * 32 + lane;
+    const int wtid = row;                      // 0..127 within the group
+    const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
+    const uint32_t s_addr = lane_base + (uint32_t)(t * 128);
+    const uint32_t o_addr = lane_base + 256u + (uint32_t)(t * 128);
+    const float sl2 = P.scale_log2;
+    const uint64_t once = ptx::policy_evict_first();
+    float* comp_t = comp_s + t * 128;
+    uint8_t* q_dst = q_s + t * C::Q_BYTES;
+    auto load_q = [&](int64_t bid) {   // one thread of the group
+      const TileDesc nt = decode_tile(P, bid);
+      ptx::mbar_expect_tx(q_full + t, C::Q_BYTES);
+#pragma unroll
+      for (int p = 0; p < 2; ++p)
+        ptx::tma_load_3d_hint(q_dst + p * C::PANEL, &tm_q, q_full + t, 64 * p, (int)nt.q_row0, (int)nt.h, once);
+    };
+    const int64_t stride = 2 * (int64_t)gridDim.x;
+    int64_t bid = 2 * (int64_t)blockIdx.x + t;
+    if (wtid == 0 && bid < n_tiles) {
+      ptx::prefetch_tmap(&tm_q);
+      load_q(bid);
+    }
+    uint32_t ns = 0, no = 0, nq = 0;   // s_full / o_full / q_full phases seen by this group
+    int tr = 0;   // trace index (RSA_PAIR_TRACE)
+    (void)tr;
+    for (; bid < n_tiles; bid += stride, ++nq) {
+      const TileDesc T = decode_tile(P, bid);
+      const int count = (int)T.count;
+      const bool next = bid + stride < n_tiles;
+      // park this tile's compensation row (the previous epilogue's readers are done)
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + t) : "memory");
+      float rpre = 1.f;
+      if (P.rectify && !T.text) {
+        const int64_t n_blk = T.q_row0 / g.B;
+        comp_t[row] = (float)P.ws.comp[(T.h * g.N + n_blk) * D + row];
+        rpre = P.ws.r_eff[T.h * g.N + n_blk];
+      }
+      const int32_t* list = T.list;
+      const int m_first = (int)T.m_first;
+      float m_run = -INFINITY, l_run = 0.f;
+      int32_t ent_next = (list && count > 0) ? list[0] : 0;
+      for (int j = 0; j < count; ++j) {
+        const int m = list ? (ent_next & 0xFFFFFF) : m_first + j;
+        if (list && j + 1 < count) ent_next = list[j + 1];
+        const int len = (int)kv_len(g, m);
+        if (wtid == 0) PAIR_TRACE(1 + t, tr, clock64());
+        ptx::mbar_wait(s_full + t, ns & 1u);
+        ++ns;
+        ptx::tc_fence_after();
+        if (wtid == 0) PAIR_TRACE(1 + t, tr + 1, clock64());
+        // the tile's last S has read Q_t: bring in the next tile's Q now
+        if (j == count - 1 && next && wtid == 0) load_q(bid + stride);
+        uint32_t sr[4][32];
+        float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        const float2 sc2 = make_float2(sl2, sl2);
+        // P = 2^(s * scale - base) of 32 columns -> bf16 pairs in TMEM columns [16c, 16c + 16)
+        auto exp_chunk = [&](int c, float2 nb2) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float2 x = ptx::ffma2(make_float2(__uint_as_float(sr[c][2 * i]), __uint_as_float(sr[c][2 * i + 1])),
+                                        sc2, nb2);
+            const float2 p = (i < RSA_PAIR_POLY) ? ptx::ex2_poly2(x) : make_float2(ptx::ex2(x.x), ptx::ex2(x.y));
+            sum2[i & 1] = ptx::fadd2(sum2[i & 1], p);
+            pk[i] = ptx::pack_bf16(p.x, p.y);
+          }
+          ptx::tmem_st16(s_addr + c * 16, pk);
+        };
+        auto max2 = [&](int c0_, float mx) {   // max over columns [32 c0_, 32 c0_ + 64)
+          float a4[4] = {mx, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+          for (int c = c0_; c < c0_ + 2; ++c)
+#pragma unroll
+            for (int i = 0; i < 32; ++i) a4[i & 3] = fmaxf(a4[i & 3], __uint_as_float(sr[c][i]));
+          return fmaxf(fmaxf(a4[0], a4[1]), fmaxf(a4[2], a4[3]));
+        };
+        float alpha = 1.f;
+        bool rescale_o = false;
+        ptx::tmem_ld32(s_addr, sr[0]);
+        ptx::tmem_ld32(s_addr + 32, sr[1]);
+        ptx::tmem_ld_wait();
+        if (wtid == 0) PAIR_TRACE(1 + t, tr + 2, clock64());
+        if (len == 128 && __all_sync(0xffffffffu, m_run != -INFINITY)) {
+          // Speculative: exponentiate against the running base m_run while the
+          // block max is still being found, and the second half of S is still
+          // loading.  The lazy-rescale rule keeps m_run unless the block max
+          // exceeds it by more than 2^kRescaleThreshold -- then (rarely, and
+          // warp-wide because tcgen05.st is warp-collective) redo all four
+          // chunks against the new base.  Same decisions and bases as the
+          // max-first path, so the same P bits.
+          ptx::tmem_ld32(s_addr + 64, sr[2]);
+          ptx::tmem_ld32(s_addr + 96, sr[3]);
+          const float2 nb2 = make_float2(-m_run, -m_run);
+          if (wtid == 0) PAIR_TRACE(1 + t, tr + 3, clock64());
+          exp_chunk(0, nb2);
+          exp_chunk(1, nb2);
+          float mx = max2(0, -INFINITY);
+          ptx::tmem_ld_wait();
+          exp_chunk(2, nb2);
+          exp_chunk(3, nb2);
+          mx = max2(2, mx);
+          const float m_blk = mx * sl2;
+          const bool redo = m_blk > m_run + kRescaleThreshold;
+          if (__any_sync(0xffffffffu, redo)) {
+            if (redo) {
+              alpha = ptx::ex2(m_run - m_blk);
+              rescale_o = true;
+              m_run = m_blk;
+            }
+            sum2[0] = sum2[1] = make_float2(0.f, 0.f);
+            const float2 nb = make_float2(-m_run, -m_run);
+            ptx::tmem_st_wait();   // the speculative P stores land before they are overwritten
+#pragma unroll
+            for (int c = 0; c < 4; ++c) exp_chunk(c, nb);
+          }
+        } else {
+          // first block of the tile (or a ragged block): row max first
+          ptx::tmem_ld32(s_addr + 64, sr[2]);
+          ptx::tmem_ld32(s_addr + 96, sr[3]);
+          ptx::tmem_ld_wait();
+          if (len < 128) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (c * 32 + i >= len) sr[c][i] = __float_as_uint(-INFINITY);
+          }
+          const float m_blk = max2(2, max2(0, -INFINITY)) * sl2;
+          if (m_blk > m_run + kRescaleThreshold || (m_run == -INFINITY && m_blk > -INFINITY)) {
+            alpha = (m_run == -INFINITY) ? 0.f : ptx::ex2(m_run - m_blk);
+            rescale_o = (m_run != -INFINITY) && j > 0;
+            m_run = m_blk;
+          }
+          const float base_m = (m_run == -INFINITY) ? 0.f : m_run;
+          const float2 nb2 = make_float2(-base_m, -base_m);
+          if (wtid == 0) PAIR_TRACE(1 + t, tr + 3, clock64());
+#pragma unroll
+          for (int c = 0; c < 4; ++c) exp_chunk(c, nb2);
+        }
+        if (__any_sync(0xffffffffu, rescale_o)) {
+          // O_t holds exactly PV_t_0 .. PV_t_{j-1} (this s_full phase implies
+          // it) and PV_t_j waits for the P release below
+          const float a = rescale_o ? alpha : 1.f;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t o[32];
+            ptx::tmem_ld32(o_addr + c * 32, o);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * a);
+            ptx::tmem_st32(o_addr + c * 32, o);
+          }
+        }
+        if (wtid == 0) PAIR_TRACE(1 + t, tr + 4, clock64());
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(p_full + t);
+        if (wtid == 0) PAIR_TRACE(1 + t, tr + 5, clock64());
+        tr += 6;
+        const float2 st2 = ptx::fadd2(sum2[0], sum2[1]);
+        l_run = l_run * alpha + (st2.x + st2.y);
+      }
+      if (count == 0) {
+        // empty kv list: no S read Q_t; once its load has landed the next Q
+        // can go in.  One P phase tells the MMA warp this group is past its
+        // previous epilogue.
+        if (next && wtid == 0) {
+          ptx::mbar_wait(q_full + t, nq & 1u);
+          load_q(bid + stride);
+        }
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(p_full + t);
+      }
+      // ---- epilogue: O / l, rectification (rectify.py:66-89), bf16 store, LSE ----
+      ptx::mbar_wait(o_full + t, no & 1u);
+      ++no;
+      ptx::tc_fence_after();
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + t) : "memory");   // the parked compensation row
+      const bool valid = row < T.rows_valid;
+      const int64_t grow = T.q_row0 + row;
+      if (T.text) {
+        float* po = P.text_part + (T.part * 128 + row) * D;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t o[32];
+          ptx::tmem_ld32(o_addr + c * 32, o);
+          ptx::tmem_ld_wait();
+          if (valid) {
+#pragma unroll
+            for (int v4 = 0; v4 < 8; ++v4)
+              *reinterpret_cast<uint4*>(po + c * 32 + v4 * 4) =
+                  make_uint4(o[v4 * 4], o[v4 * 4 + 1], o[v4 * 4 + 2], o[v4 * 4 + 3]);
+          }
+        }
+        if (valid) P.text_ml[T.part * 128 + row] = make_float2(m_run, l_run);
+      } else {
+        const float rfac = (P.rectify && valid) ? rpre : 1.f;
+        const bool comp = P.rectify && valid;
+        const float inv_l = (count > 0 && l_run > 0.f) ? 1.f / l_run : 0.f;
+        const int64_t orig = (P.perm && valid) ? P.perm[grow] : grow;
+        __nv_bfloat16* orow = P.out + (T.h * g.T + orig) * D;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t o[32];
+          ptx::tmem_ld32(o_addr + c * 32, o);
+          ptx::tmem_ld_wait();
+          if (valid) {
+#pragma unroll
+            for (int v8 = 0; v8 < 4; ++v8) {
+              uint32_t w[4];
+#pragma unroll
+              for (int q2 = 0; q2 < 4; ++q2) {
+                const int col = c * 32 + v8 * 8 + 2 * q2;
+                float y0 = inv_l == 0.f ? 0.f : __uint_as_float(o[v8 * 8 + 2 * q2]) * inv_l * rfac;
+                float y1 = inv_l == 0.f ? 0.f : __uint_as_float(o[v8 * 8 + 2 * q2 + 1]) * inv_l * rfac;
+                if (comp) {
+                  y0 += comp_t[col];
+                  y1 += comp_t[col + 1];
+                }
+                w[q2] = ptx::pack_bf16(y0, y1);
+              }
+              ptx::st_stream(orow + c * 32 + v8 * 8, make_uint4(w[0], w[1], w[2], w[3]), once);
+            }
+          }
+        }
+        if (valid && P.lse)
+          P.lse[T.h * g.T + orig] = l_run > 0.f ? (log2f(l_run) + m_run) * 0.69314718055994531f : -INFINITY;
+      }
+      // the O_t reads above complete before this group's next P_t release
+      ptx::tc_fence_before();
+    }
+  }
+
+  __syncwarp();
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tmem);
+  }
+}
+
+cudaError_t launch_pair(const Geometry& g, const void* q, const void* k, const void* v, void* out, float* lse,
+                        const Workspace& ws, bool rectify, bool text, cudaStream_t st, const int32_t* perm) {
+  using C = CfgPair;
+  CUtensorMap tq, tk, tv;
+  if (!make_tmap_3d(&tq, q, g.d, g.T, g.H, 128) || !make_tmap_3d(&tk, k, g.d, g.T, g.H, 128) ||
+      !make_tmap_3d(&tv, v, g.d, g.T, g.H, 128))
+    return cudaErrorInvalidValue;
+  TcParams P{};
+  P.g = g;
+  P.ws = ws;
+  P.out = static_cast<__nv_bfloat16*>(out);
+  P.q = static_cast<const __nv_bfloat16*>(q);
+  P.lse = lse;
+  P.perm = perm;   // (q is then the permuted copy; outputs are scattered back)
+  P.rectify = rectify ? 1 : 0;
+  P.text_tiles_per_head = text ? (g.Tt + 127) / 128 : 0;
+  P.text_chunks = text_chunks(g);
+  P.chunk_blocks = (g.M + P.text_chunks - 1) / P.text_chunks;
+  P.video_tiles_per_head = (g.N * g.B + 127) / 128;
+  P.tiles_per_head = P.text_tiles_per_head * P.text_chunks + P.video_tiles_per_head;
+  P.text_part = ws.text_part;
+  P.text_ml = reinterpret_cast<float2*>(ws.text_ml);
+  P.scale_log2 = (float)(1.4426950408889634 / sqrt((double)g.d));
+  cudaError_t e = cudaFuncSetAttribute(attn_tc_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t n_tiles = g.H * P.tiles_per_head;
+  attn_tc_pair_kernel<<<(unsigned)std::min<int64_t>((n_tiles + 1) / 2, sms), C::THREADS, C::SMEM, st>>>(
+      tq, tk, tv, P, n_tiles);
+  e = cudaGetLastError();
+  if (e != cudaSuccess || P.text_tiles_per_head == 0) return e;
+  text_combine_kernel<128><<<(unsigned)(g.H * P.text_tiles_per_head), 256, 0, st>>>(
+      P.text_part, P.text_ml, P.out, lse, g, P.text_tiles_per_head, P.text_chunks);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_pp(const Geometry& g, const void* q, const void* k, const void* v, void* out, float* lse,
                       const Workspace& ws, bool rectify, bool text, cudaStream_t st, const int32_t* perm) {
   using C = CfgPP;
@@ -1045,6 +1648,12 @@ cudaError_t launch_persistent(const Geometry& g, const void* q, const void* k, c
 
 }  // namespace
 
+#ifdef RSA_PAIR_TRACE
+extern "C" int rsa_debug_pair_trace(long long* dst, int n) {
+  return (int)cudaMemcpyFromSymbol(dst, g_pair_trace, sizeof(long long) * (size_t)std::min(n, 4 * 16384));
+}
+#endif
+
 bool tc_supported(const Geometry& g) {
   return g.dtype == RSA_BF16 && (g.d == 64 || g.d == 128) && (g.B == 64 || g.B == 128) &&
          g.T * g.d < (int64_t(1) << 31) && g.H < 65536 && tmap_encode_fn() != nullptr;
@@ -1057,8 +1666,11 @@ cudaError_t launch_attn_tc(const Geometry& g, const void* q, const void* k, cons
   // d = B = 128: the ping-pong kernel (the permuted problem runs on it with the
   // permuted Q copy K1 wrote); RSA_KERNEL_TCGEN05_PERSISTENT asks for the
   // one-tile persistent kernel instead (cross-checks)
-  if (g.d == 128 && g.B == 128 && kernel != RSA_KERNEL_TCGEN05_PERSISTENT && (!perm || q_perm))
-    return launch_pp(g, perm ? q_perm : q, k, v, out, lse, ws, rectify, text, st, perm);
+  if (g.d == 128 && g.B == 128 && kernel != RSA_KERNEL_TCGEN05_PERSISTENT && (!perm || q_perm)) {
+    if (kernel == RSA_KERNEL_TCGEN05_PINGPONG)
+      return launch_pp(g, perm ? q_perm : q, k, v, out, lse, ws, rectify, text, st, perm);
+    return launch_pair(g, perm ? q_perm : q, k, v, out, lse, ws, rectify, text, st, perm);
+  }
 #define RSA_TC_P(DD, BB) \
   if (g.d == DD && g.B == BB) return launch_persistent<DD, BB, 2>(g, q, k, v, out, lse, ws, rectify, text, st, perm);
   RSA_TC_P(128, 128)

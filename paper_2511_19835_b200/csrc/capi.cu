@@ -161,7 +161,7 @@ rsa_status run_attention(const rsa_shape* s, const rsa::Geometry& g, const rsa::
   // reference's fp32/fp64 precisions, and bf16 only when asked for by name
   // (a cross-check) -- never as a silent second backend
   if ((s->kernel == RSA_KERNEL_TCGEN05 || s->kernel == RSA_KERNEL_TCGEN05_PERSISTENT ||
-       (s->kernel == RSA_KERNEL_AUTO && g.dtype == RSA_BF16)) && !tc)
+       s->kernel == RSA_KERNEL_TCGEN05_PINGPONG || (s->kernel == RSA_KERNEL_AUTO && g.dtype == RSA_BF16)) && !tc)
     return fail(RSA_ERR_UNSUPPORTED, "bf16 attention runs on the tcgen05 kernel, which needs block and "
                                      "head_dim in {64, 128} (kernel='simt' selects the CUDA-core kernel "
                                      "explicitly)");

@@ -491,18 +491,25 @@ def test_non_finite_inputs_raise_shape_error(dtype, where):
                                            sparsity=0.5, check_status=True)
 
 
-def test_pingpong_and_persistent_k3_agree():
-    """d = B = 128 runs the ping-pong K3 by default; kernel="tcgen05-persistent"
-    selects the one-tile persistent K3 (a cross-check, never chosen silently):
-    both within the bf16 bar of each other and of the oracle."""
+@pytest.mark.parametrize("heads", [1, 12])
+def test_pair_pingpong_and_persistent_k3_agree(heads):
+    """d = B = 128 runs the paired-tile K3 by default; kernel="tcgen05-pingpong"
+    and "tcgen05-persistent" select the two-slot ping-pong and the one-tile
+    persistent K3 (cross-checks, never chosen silently): all within the bf16
+    bar of each other and of the oracle.  12 heads put ~2 tile pairs on every
+    CTA (pairs straddle heads and the text/video boundary)."""
     qv, qt, k, v = (O.round_to_bf16(x) for x in O.gen_synthetic(5, 128 * 20, 200, 128, 128, (1, 40, 64), 1.0, 2.0, 0.3))
-    q = torch.cat([to_bf16_tensor(qv), to_bf16_tensor(qt)])[None]
+    q = torch.cat([to_bf16_tensor(qv), to_bf16_tensor(qt)])[None].expand(heads, -1, -1).contiguous()
+    kk = to_bf16_tensor(k)[None].expand(heads, -1, -1).contiguous()
+    vv = to_bf16_tensor(v)[None].expand(heads, -1, -1).contiguous()
     outs = {}
-    for kern in ("tcgen05", "tcgen05-persistent"):
-        outs[kern] = rsa.rectified_sparse_attention(q, to_bf16_tensor(k)[None], to_bf16_tensor(v)[None],
-                                                    num_text_tokens=200, block=128, top_k_fraction=0.2,
-                                                    kernel=kern)[0].float().cpu().numpy().astype(np.float64)
+    for kern in ("tcgen05", "tcgen05-pingpong", "tcgen05-persistent"):
+        o = rsa.rectified_sparse_attention(q, kk, vv, num_text_tokens=200, block=128, top_k_fraction=0.2,
+                                           kernel=kern).float().cpu().numpy().astype(np.float64)
+        assert all(np.array_equal(o[0], o[h]) for h in range(heads)), kern   # identical heads
+        outs[kern] = o[0]
     assert np.abs(outs["tcgen05"] - outs["tcgen05-persistent"]).max() <= 2e-2
+    assert np.abs(outs["tcgen05"] - outs["tcgen05-pingpong"]).max() <= 2e-2
     ref = O.pipeline(qv, qt, k, v, 128, 0.2, 0.0, 0, False, "sparse-rectified")
     want = np.concatenate([ref["o_video"], ref["o_text"]])
     for kern, got in outs.items():
