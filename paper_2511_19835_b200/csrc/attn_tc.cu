@@ -423,9 +423,14 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
         }
         const float2 st2 = ptx::fadd2(sum2[0], sum2[1]);
         l_part = l_part * alpha + (st2.x + st2.y);
+        // Every pv_done phase is observed here (the one before the next PV's
+        // commit): the rescale below needs O = PV_0..PV_{j-1} of this tile, and
+        // an mbarrier phase nobody waits on is a synchronisation hazard
+        // (compute-sanitizer synccheck).  PV_{gj-1} ran right behind S_gj, so
+        // after the exps above the wait is normally already satisfied.
+        if (gj >= 1) ptx::mbar_wait(pv_done, (uint32_t)((gj - 1) & 1));
         if (__any_sync(0xffffffffu, rescale_o)) {
           // O must hold exactly PV_0..PV_{j-1} of this tile before it is rescaled
-          ptx::mbar_wait(pv_done, (uint32_t)((gj - 1) & 1));
           ptx::tc_fence_after();
           const float a = rescale_o ? alpha : 1.f;
 #pragma unroll
@@ -868,8 +873,9 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
         }
         const float2 st2 = ptx::fadd2(sum2[0], sum2[1]);
         l_run = l_run * alpha + (st2.x + st2.y);
+        // every pv_done phase is observed (see the persistent kernel)
+        if (gsub >= 1) ptx::mbar_wait(slot_bar(s, 8), (uint32_t)((gsub - 1) & 1));   // O = PV_..i-1
         if (__any_sync(0xffffffffu, rescale_o)) {
-          ptx::mbar_wait(slot_bar(s, 8), (uint32_t)((gsub - 1) & 1));   // O = PV_..i-1
           ptx::tc_fence_after();
           const float a = rescale_o ? alpha : 1.f;
 #pragma unroll

@@ -9,7 +9,37 @@
 
 using namespace rsa;
 
-// VAR: 0 full loop, 1 pack by PRMT (no F2FP), 2 no row sum, 3 no pack and no sum
+// VAR: 0 full loop, 1 pack by PRMT (no F2FP), 2 no row sum, 3 no pack and no sum,
+//      4 phased: all FFMA2 of a chunk, then all ex2, then packs and sums
+//      5 software-pipelined: pack/sum of pair i after the ex2 of pair i + LAG (asm volatile order)
+template <int LAG>
+__device__ __forceinline__ void exp_pipelined(float* v, float2 sc2, float2 nb2, float2* sum2, uint32_t* pk) {
+  // v[32]: scores in, 2^x in place; pk[16] bf16 pairs; FFMA2 two pairs ahead, pack/sum LAG pairs behind
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float2 x = ptx::ffma2(make_float2(v[2 * i], v[2 * i + 1]), sc2, nb2);
+    v[2 * i] = x.x; v[2 * i + 1] = x.y;
+  }
+#pragma unroll
+  for (int i = 0; i < 16 + LAG; ++i) {
+    if (i < 16) {
+      asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(v[2 * i]));
+      asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(v[2 * i + 1]));
+    }
+    if (i + 2 < 16) {
+      const float2 x = ptx::ffma2(make_float2(v[2 * i + 4], v[2 * i + 5]), sc2, nb2);
+      v[2 * i + 4] = x.x; v[2 * i + 5] = x.y;
+    }
+    if (i >= LAG) {
+      const int q = i - LAG;
+      uint32_t r;
+      asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(v[2 * q + 1]), "f"(v[2 * q]));
+      pk[q] = r;
+      sum2[q & 1] = ptx::fadd2(sum2[q & 1], make_float2(v[2 * q], v[2 * q + 1]));
+    }
+  }
+}
+
 template <int POLY, int VAR = 0>
 __global__ void k(const float* in, uint32_t* out, int iters) {
   float s[128];
@@ -22,6 +52,50 @@ __global__ void k(const float* in, uint32_t* out, int iters) {
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       uint32_t pk[16];
+      if (VAR >= 6) {
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = s[32 * c + i];
+        if (VAR == 6) exp_pipelined<2>(v, sc2, nb2, sum2, pk);
+        if (VAR == 7) exp_pipelined<3>(v, sc2, nb2, sum2, pk);
+        if (VAR == 8) exp_pipelined<4>(v, sc2, nb2, sum2, pk);
+      } else if (VAR == 5) {
+        constexpr int LAG = 2;
+        float2 xs[16], ps[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) xs[i] = ptx::ffma2(make_float2(s[32 * c + 2 * i], s[32 * c + 2 * i + 1]), sc2, nb2);
+#pragma unroll
+        for (int i = 0; i < 16 + LAG; ++i) {
+          if (i < 16) {
+            float a = xs[i].x, b = xs[i].y;
+            asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a));
+            asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(b));
+            ps[i] = make_float2(a, b);
+          }
+          if (i >= LAG) {
+            const int q = i - LAG;
+            uint32_t r;
+            asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(ps[q].y), "f"(ps[q].x));
+            pk[q] = r;
+            sum2[q & 1] = ptx::fadd2(sum2[q & 1], ps[q]);
+          }
+        }
+      } else if (VAR == 4) {
+        float xv[32];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float2 x = ptx::ffma2(make_float2(s[32 * c + 2 * i], s[32 * c + 2 * i + 1]), sc2, nb2);
+          xv[2 * i] = x.x; xv[2 * i + 1] = x.y;
+        }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(xv[i]));
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float2 p = make_float2(xv[2 * i], xv[2 * i + 1]);
+          sum2[i & 1] = ptx::fadd2(sum2[i & 1], p);
+          pk[i] = ptx::pack_bf16(p.x, p.y);
+        }
+      } else
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const float2 x = ptx::ffma2(make_float2(s[32 * c + 2 * i], s[32 * c + 2 * i + 1]), sc2, nb2);
@@ -54,6 +128,16 @@ int main() {
     k<0, 2><<<148, warps * 32>>>(in, out, 2000); cudaDeviceSynchronize();
     printf("warps/SM %d, no pack, no sum:\n", warps);
     k<0, 3><<<148, warps * 32>>>(in, out, 2000); cudaDeviceSynchronize();
+    printf("warps/SM %d, phased (FFMA2s, ex2s, packs):\n", warps);
+    k<0, 4><<<148, warps * 32>>>(in, out, 2000); cudaDeviceSynchronize();
+    printf("warps/SM %d, software-pipelined lag 2:\n", warps);
+    k<0, 5><<<148, warps * 32>>>(in, out, 2000); cudaDeviceSynchronize();
+    printf("warps/SM %d, in-place pipelined lag 2:\n", warps);
+    k<0, 6><<<148, warps * 32>>>(in, out, 2000); cudaDeviceSynchronize();
+    printf("warps/SM %d, in-place pipelined lag 3:\n", warps);
+    k<0, 7><<<148, warps * 32>>>(in, out, 2000); cudaDeviceSynchronize();
+    printf("warps/SM %d, in-place pipelined lag 4:\n", warps);
+    k<0, 8><<<148, warps * 32>>>(in, out, 2000); cudaDeviceSynchronize();
     printf("warps/SM %d, poly 2/16:\n", warps);
     k<2><<<148, warps * 32>>>(in, out, 2000); cudaDeviceSynchronize();
     printf("warps/SM %d, poly 4/16:\n", warps);
