@@ -164,6 +164,33 @@ rsa_status rsa_forward(const rsa_shape* shape, const rsa_config* cfg, const void
                        const void* k, const void* v, void* out, float* lse,
                        void* workspace, void* stream);
 
+/* Element strides of Q, K, V and O for rsa_forward_strided (head_dim is
+ * contiguous): head h of the call is head (h % heads_per_batch) of batch entry
+ * (h / heads_per_batch), and its token row t starts at element
+ *   (h / heads_per_batch) * batch_stride + (h % heads_per_batch) * head_stride
+ *   + t * token_stride.
+ * Contiguous [B, H, T, d]: {H, d, T d, H T d}.  A model's [B, T, H, d]
+ * projection output, without a transpose: {H, H d, d, T H d}. */
+typedef struct {
+  int64_t heads_per_batch;
+  int64_t token_stride;
+  int64_t head_stride;
+  int64_t batch_stride;
+} rsa_layout;
+
+/* rsa_forward on strided views: `layout` for Q, K and V, `out_layout` for O
+ * (NULL: the same as `layout`); `lse` and the workspace keep their [heads][T] /
+ * rsa_workspace_layout shapes.  bf16 with
+ * the tcgen05 kernels (block and head_dim in {64, 128}); strides multiples of
+ * 8 elements and 16-byte aligned pointers, else RSA_ERR_UNSUPPORTED.  K1 and
+ * K3 read the rows through 4-D TMA maps and K3 stores through the same
+ * strides: no transpose or contiguous copy is made.  The reference's arrays
+ * are 2-D [T, d] (core.py:51-57); this is the batched model-facing form of
+ * the same call. */
+rsa_status rsa_forward_strided(const rsa_shape* shape, const rsa_config* cfg, const rsa_layout* layout,
+                               const rsa_layout* out_layout, const void* q, const void* k, const void* v,
+                               void* out, float* lse, void* workspace, void* stream);
+
 /* rsa_forward from HOST memory (end-to-end call): host_q/k/v/out are host
  * pointers (page-locked for the copies to overlap), dq/dk/dv/dout device
  * buffers of the same [heads][T][d] size.  Heads are processed in chunks of

@@ -21,7 +21,8 @@ VARIANT_CODES = {"full": 0, "sparse-unrectified": 1, "sparse-rectified": 2,
 KERNEL_CODES = {"auto": 0, "tcgen05": 1, "simt": 2, "tcgen05-persistent": 3, "tcgen05-pingpong": 4}
 
 EXPORTS = ("rsa_plan", "rsa_workspace_layout_query", "rsa_workspace_size", "rsa_pool",
-           "rsa_select", "rsa_attention", "rsa_forward", "rsa_forward_host", "rsa_block_sparse_attention",
+           "rsa_select", "rsa_attention", "rsa_forward", "rsa_forward_strided", "rsa_forward_host",
+           "rsa_block_sparse_attention",
            "rsa_text_full_attention", "rsa_morton_permutation", "rsa_permute_rows",
            "rsa_permuted_buffer_size", "rsa_forward_permuted", "rsa_diagnostics_scratch_size", "rsa_diagnostics",
            "rsa_dense_reference_scratch_size", "rsa_dense_reference",
@@ -60,6 +61,12 @@ class Layout(C.Structure):
     _fields_ = [(n, C.c_size_t) for n in LAYOUT_FIELDS]
 
 
+class TensorLayout(C.Structure):
+    """rsa_layout: element strides of strided Q/K/V/O (head_dim contiguous)."""
+    _fields_ = [("heads_per_batch", C.c_int64), ("token_stride", C.c_int64), ("head_stride", C.c_int64),
+                ("batch_stride", C.c_int64)]
+
+
 _LIB = None
 
 
@@ -84,6 +91,8 @@ def lib() -> C.CDLL:
         "rsa_select": ([C.POINTER(Shape), C.POINTER(Config), P, P], C.c_int),
         "rsa_attention": ([C.POINTER(Shape), C.POINTER(Config), P, P, P, P, P, P, P], C.c_int),
         "rsa_forward": ([C.POINTER(Shape), C.POINTER(Config), P, P, P, P, P, P, P], C.c_int),
+        "rsa_forward_strided": ([C.POINTER(Shape), C.POINTER(Config), C.POINTER(TensorLayout),
+                                 C.POINTER(TensorLayout), P, P, P, P, P, P, P], C.c_int),
         "rsa_forward_host": ([C.POINTER(Shape), C.POINTER(Config), P, P, P, P, P, P, P, P, P, P,
                               C.c_int64, P], C.c_int),
         "rsa_block_sparse_attention": ([C.POINTER(Shape), P, P, P, P, P, P, P, P], C.c_int),

@@ -83,6 +83,15 @@ struct TcParams {
 // per-CTA launch gap (~8 us), set-up and Q-load latency of the one-tile
 // kernel (profiles/r01j: 16 us of ~117 us per tile).
 // ============================================================================
+// 64 columns x box rows of head h starting at token row `row` (4-D tensor
+// maps over (d, T, head of the batch entry, batch entry): any row-contiguous
+// [B, H, T, d] or [B, T, H, d] view, see make_rows_tmap)
+__device__ __forceinline__ void tma_rows(void* dst, const CUtensorMap* tm, uint64_t* bar, int col, int row, int64_t h,
+                                         const Geometry& g, uint64_t policy) {
+  const int hb = (int)g.hb, hh = (int)h;
+  ptx::tma_load_4d_hint(dst, tm, bar, col, row, hh % hb, hh / hb, policy);
+}
+
 struct TileDesc {
   int64_t h, q_row0, rows_valid, count, m_first, part;
   const int32_t* list;
@@ -148,7 +157,7 @@ __device__ __forceinline__ void producer_loop(const CUtensorMap& tm_q, const CUt
         uint8_t* dst = kv_s + s * C::STAGE;
 #pragma unroll
         for (int p = 0; p < C::PANELS; ++p)
-          ptx::tma_load_3d_hint(dst + p * C::Q_PANEL, &tm_q, kv_full + s, 64 * p, (int)t.q_row0, (int)t.h, once);
+          tma_rows(dst + p * C::Q_PANEL, &tm_q, kv_full + s, 64 * p, (int)t.q_row0, (int)t.h, g, once);
         if (++s == C::NST) { s = 0; ph ^= 1; }
       }
       auto load = [&](int64_t j, bool is_v) {
@@ -158,8 +167,8 @@ __device__ __forceinline__ void producer_loop(const CUtensorMap& tm_q, const CUt
         uint8_t* dst = kv_s + s * C::STAGE;
 #pragma unroll
         for (int p = 0; p < C::PANELS; ++p)
-          ptx::tma_load_3d_hint(dst + p * C::KV_PANEL, is_v ? &tm_v : &tm_k, kv_full + s, 64 * p,
-                                (int)kv_row0(g, m), (int)t.h, keep);
+          tma_rows(dst + p * C::KV_PANEL, is_v ? &tm_v : &tm_k, kv_full + s, 64 * p, (int)kv_row0(g, m), t.h, g,
+                   keep);
         if (++s == C::NST) { s = 0; ph ^= 1; }
       };
       for (int64_t j = 0; j <= t.count; ++j) {
@@ -332,7 +341,7 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
         const int64_t grow = t.q_row0 + row;
         // permuted problem: gather the query row from its original position
         const int64_t srow = (P.perm && grow < g.Tv) ? P.perm[grow] : grow;
-        const uint4* src = reinterpret_cast<const uint4*>(P.q + (t.h * g.T + srow) * D + half * (D / WPQ));
+        const uint4* src = reinterpret_cast<const uint4*>(P.q + row_off(g, t.h, srow) + half * (D / WPQ));
 #pragma unroll
         for (int i = 0; i < QW / 4; ++i) {
           const uint4 x = grow < g.T ? ptx::ld_stream(src + i, once) : make_uint4(0, 0, 0, 0);
@@ -495,7 +504,7 @@ attn_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid
         const float inv_l = (count > 0 && l_run > 0.f) ? 1.f / l_run : 0.f;
         // permuted problem: scatter the row back to its original position
         const int64_t orig = (P.perm && valid) ? P.perm[grow] : grow;
-        __nv_bfloat16* orow = P.out + (cur.h * g.T + orig) * D;
+        __nv_bfloat16* orow = P.out + out_off(g, cur.h, orig);
 #pragma unroll
         for (int c = 0; c < HD / 32; ++c) {
           uint32_t o[32];
@@ -571,7 +580,7 @@ __global__ void __launch_bounds__(256) text_combine_kernel(const float* __restri
     }
   }
   const float inv = l > 0.f ? 1.f / l : 0.f;
-  __nv_bfloat16* orow = out + (h * g.T + g.Tv + trow) * D + half * (D / 2);
+  __nv_bfloat16* orow = out + out_off(g, h, g.Tv + trow) + half * (D / 2);
 #pragma unroll
   for (int i = 0; i < D / 16; ++i) {
     uint32_t w[4];
@@ -582,22 +591,6 @@ __global__ void __launch_bounds__(256) text_combine_kernel(const float* __restri
   if (lse && half == 0) lse[h * g.T + g.Tv + trow] = l > 0.f ? (log2f(l) + mx) * 0.69314718055994531f : -INFINITY;
 }
 
-
-// 3-D bf16 tensor [dim2][dim1][dim0] (dim0 contiguous), box (64, box1, 1), 128B swizzle
-bool make_tmap_3d(CUtensorMap* tm, const void* ptr, int64_t dim0, int64_t dim1, int64_t dim2, int box1,
-                  int64_t pitch0 = 0) {
-  auto fn = tmap_encode_fn();
-  if (!fn) return false;
-  if (pitch0 == 0) pitch0 = dim0;
-  cuuint64_t dims[3] = {(cuuint64_t)dim0, (cuuint64_t)dim1, (cuuint64_t)dim2};
-  cuuint64_t strides[2] = {(cuuint64_t)pitch0 * 2, (cuuint64_t)dim1 * pitch0 * 2};
-  cuuint32_t box[3] = {64, (cuuint32_t)box1, 1};
-  cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
 
 // ============================================================================
 // Ping-pong kernel (d = B = 128): two query tiles per CTA in
@@ -683,8 +676,8 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
         ptx::mbar_expect_tx(slot_bar(s, 0), C::Q_BYTES);
 #pragma unroll
         for (int p = 0; p < 2; ++p)
-          ptx::tma_load_3d_hint(qs + p * C::Q_PANEL, &tm_q, slot_bar(s, 0), 64 * p, (int)t.q_row0, (int)t.h,
-                                once);   // Q rows are read by one tile: keep L2 for K/V
+          tma_rows(qs + p * C::Q_PANEL, &tm_q, slot_bar(s, 0), 64 * p, (int)t.q_row0, t.h, g,
+                   once);   // Q rows are read by one tile: keep L2 for K/V
         for (int64_t j = 0; j < t.count; ++j) {
           const int64_t m = t.list ? (t.list[j] & 0xFFFFFF) : t.m_first + j;
 #pragma unroll
@@ -694,8 +687,8 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
             uint8_t* dst = ring + st * C::STAGE;
 #pragma unroll
             for (int p = 0; p < 2; ++p)
-              ptx::tma_load_3d_hint(dst + p * C::KV_PANEL, kv ? &tm_v : &tm_k, slot_bar(s, 2 + st), 64 * p,
-                                    (int)kv_row0(g, m), (int)t.h, keep);
+              tma_rows(dst + p * C::KV_PANEL, kv ? &tm_v : &tm_k, slot_bar(s, 2 + st), 64 * p, (int)kv_row0(g, m),
+                       t.h, g, keep);
             if (++st == C::NST) { st = 0; ph ^= 1; }
           }
         }
@@ -924,7 +917,7 @@ attn_tc_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
         const float inv_l = (nsub > 0 && l_run > 0.f) ? 1.f / l_run : 0.f;
         // permuted problem: scatter the row back to its original position
         const int64_t orig = (P.perm && valid) ? P.perm[grow] : grow;
-        __nv_bfloat16* orow = P.out + (t.h * g.T + orig) * D;
+        __nv_bfloat16* orow = P.out + out_off(g, t.h, orig);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           uint32_t o[32];
@@ -1112,12 +1105,12 @@ attn_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
 #pragma unroll
             for (int p = 0; p < 2; ++p) {
               if (jp < c0) {
-                ptx::tma_prefetch_3d(&tm_k, 64 * p, (int)kv_row0(g, pf0), h0);
-                ptx::tma_prefetch_3d(&tm_v, 64 * p, (int)kv_row0(g, pf0), h0);
+                ptx::tma_prefetch_4d(&tm_k, 64 * p, (int)kv_row0(g, pf0), h0 % (int)g.hb, h0 / (int)g.hb);
+                ptx::tma_prefetch_4d(&tm_v, 64 * p, (int)kv_row0(g, pf0), h0 % (int)g.hb, h0 / (int)g.hb);
               }
               if (jp < c1) {
-                ptx::tma_prefetch_3d(&tm_k, 64 * p, (int)kv_row0(g, pf1), h1);
-                ptx::tma_prefetch_3d(&tm_v, 64 * p, (int)kv_row0(g, pf1), h1);
+                ptx::tma_prefetch_4d(&tm_k, 64 * p, (int)kv_row0(g, pf1), h1 % (int)g.hb, h1 / (int)g.hb);
+                ptx::tma_prefetch_4d(&tm_v, 64 * p, (int)kv_row0(g, pf1), h1 % (int)g.hb, h1 / (int)g.hb);
               }
             }
             pf0 = q0;
@@ -1141,7 +1134,7 @@ attn_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             const int row0 = (int)kv_row0(g, m), hh = tt ? h1 : h0;
 #pragma unroll
             for (int p = 0; p < 2; ++p)
-              ptx::tma_load_3d_hint(dst + p * C::PANEL, tmap, kv_full + st, 64 * p, row0, hh, keep);
+              tma_rows(dst + p * C::PANEL, tmap, kv_full + st, 64 * p, row0, hh, g, keep);
             if (++st == C::NST) { st = 0; ph ^= 1; }
           }
           m1_prev = m1;
@@ -1303,7 +1296,7 @@ attn_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
       ptx::mbar_expect_tx(q_full + t, C::Q_BYTES);
 #pragma unroll
       for (int p = 0; p < 2; ++p)
-        ptx::tma_load_3d_hint(q_dst + p * C::PANEL, &tm_q, q_full + t, 64 * p, (int)nt.q_row0, (int)nt.h, once);
+        tma_rows(q_dst + p * C::PANEL, &tm_q, q_full + t, 64 * p, (int)nt.q_row0, (int)nt.h, g, once);
     };
     const int64_t stride = 2 * (int64_t)gridDim.x;
     int64_t bid = 2 * (int64_t)blockIdx.x + t;
@@ -1489,7 +1482,7 @@ attn_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         const bool comp = P.rectify && valid;
         const float inv_l = (count > 0 && l_run > 0.f) ? 1.f / l_run : 0.f;
         const int64_t orig = (P.perm && valid) ? P.perm[grow] : grow;
-        __nv_bfloat16* orow = P.out + (T.h * g.T + orig) * D;
+        __nv_bfloat16* orow = P.out + out_off(g, T.h, orig);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           uint32_t o[32];
@@ -1535,8 +1528,9 @@ cudaError_t launch_pair(const Geometry& g, const void* q, const void* k, const v
                         const Workspace& ws, bool rectify, bool text, cudaStream_t st, const int32_t* perm) {
   using C = CfgPair;
   CUtensorMap tq, tk, tv;
-  if (!make_tmap_3d(&tq, q, g.d, g.T, g.H, 128) || !make_tmap_3d(&tk, k, g.d, g.T, g.H, 128) ||
-      !make_tmap_3d(&tv, v, g.d, g.T, g.H, 128))
+  if (!make_rows_tmap(&tq, q, g, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_rows_tmap(&tk, k, g, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_rows_tmap(&tv, v, g, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
   TcParams P{};
   P.g = g;
@@ -1573,8 +1567,9 @@ cudaError_t launch_pp(const Geometry& g, const void* q, const void* k, const voi
                       const Workspace& ws, bool rectify, bool text, cudaStream_t st, const int32_t* perm) {
   using C = CfgPP;
   CUtensorMap tq, tk, tv;
-  if (!make_tmap_3d(&tq, q, g.d, g.T, g.H, 128) || !make_tmap_3d(&tk, k, g.d, g.T, g.H, 128) ||
-      !make_tmap_3d(&tv, v, g.d, g.T, g.H, 128))
+  if (!make_rows_tmap(&tq, q, g, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_rows_tmap(&tk, k, g, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_rows_tmap(&tv, v, g, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
   TcParams P{};
   P.g = g;
@@ -1613,8 +1608,9 @@ cudaError_t launch_persistent(const Geometry& g, const void* q, const void* k, c
                               const int32_t* perm) {
   using C = Cfg<D, BKV>;
   CUtensorMap tq, tk, tv;
-  if (!make_tmap_3d(&tq, q, g.d, g.T, g.H, 128) || !make_tmap_3d(&tk, k, g.d, g.T, g.H, BKV) ||
-      !make_tmap_3d(&tv, v, g.d, g.T, g.H, BKV))
+  if (!make_rows_tmap(&tq, q, g, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_rows_tmap(&tk, k, g, 64, BKV, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_rows_tmap(&tv, v, g, 64, BKV, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
   TcParams P{};
   // Q through the ring when a Q tile is exactly one stage (BKV = 128) and rows

@@ -65,10 +65,55 @@ rsa_status make_geometry(const rsa_shape* s, rsa::Geometry* g) {
   g->s_tok = g->d;
   g->s_head = g->T * g->d;
   g->s_batch = g->H * g->T * g->d;
+  g->o_hb = g->hb; g->o_tok = g->s_tok; g->o_head = g->s_head; g->o_batch = g->s_batch;
   const int64_t dmax = s->dtype == RSA_F64 ? 128 : 256;
   if (g->d > dmax)
     return fail(RSA_ERR_UNSUPPORTED, "head_dim " + std::to_string(g->d) + " > " + std::to_string(dmax));
   if (g->M > 8192) return fail(RSA_ERR_UNSUPPORTED, "more than 8192 kv blocks");
+  return RSA_OK;
+}
+
+bool contiguous(const rsa::Geometry& g) {
+  return g.hb == g.H && g.s_tok == g.d && g.s_head == g.T * g.d && g.s_batch == g.H * g.T * g.d &&
+         g.o_hb == g.H && g.o_tok == g.d && g.o_head == g.T * g.d && g.o_batch == g.H * g.T * g.d;
+}
+
+// A strided call's element strides (rsa_layout) replace the contiguous
+// [H][T][d] default.  The strided path is the model-facing one: bf16 on the
+// tcgen05 kernels, whose TMA maps need 16-byte row / head / batch strides.
+rsa_status check_layout(const rsa_layout* l, const rsa::Geometry& g) {
+  if (l->heads_per_batch < 1 || g.H % l->heads_per_batch != 0)
+    return fail(RSA_ERR_SHAPE, "heads must be a multiple of layout.heads_per_batch");
+  if (l->token_stride < g.d || l->head_stride < 0 || l->batch_stride < 0)
+    return fail(RSA_ERR_SHAPE, "layout strides must be non-negative and token_stride >= head_dim");
+  if (l->token_stride % 8 || l->head_stride % 8 || l->batch_stride % 8)
+    return fail(RSA_ERR_UNSUPPORTED, "layout strides must be multiples of 8 elements (16-byte TMA rows)");
+  return RSA_OK;
+}
+
+// A strided call's element strides (rsa_layout) replace the contiguous
+// [H][T][d] default.  The strided path is the model-facing one: bf16 on the
+// tcgen05 kernels, whose TMA maps need 16-byte row / head / batch strides.
+rsa_status apply_layout(const rsa_layout* l, const rsa_layout* lo, const void* const* ptrs, int n_ptrs,
+                        rsa::Geometry* g) {
+  if (!l) return fail(RSA_ERR_SHAPE, "null layout");
+  if (!lo) lo = l;
+  if (g->dtype != RSA_BF16) return fail(RSA_ERR_UNSUPPORTED, "strided q/k/v/out are supported for bfloat16 only");
+  rsa_status s = check_layout(l, *g);
+  if (s != RSA_OK) return s;
+  s = check_layout(lo, *g);
+  if (s != RSA_OK) return s;
+  for (int i = 0; i < n_ptrs; ++i)
+    if (reinterpret_cast<uintptr_t>(ptrs[i]) % 16)
+      return fail(RSA_ERR_UNSUPPORTED, "strided q/k/v/out must be 16-byte aligned");
+  g->hb = l->heads_per_batch;
+  g->s_tok = l->token_stride;
+  g->s_head = l->head_stride;
+  g->s_batch = l->batch_stride;
+  g->o_hb = lo->heads_per_batch;
+  g->o_tok = lo->token_stride;
+  g->o_head = lo->head_stride;
+  g->o_batch = lo->batch_stride;
   return RSA_OK;
 }
 
@@ -172,6 +217,7 @@ rsa_status run_attention(const rsa_shape* s, const rsa::Geometry& g, const rsa::
     if (e != cudaSuccess) return cuda_fail(e, "attn_tc");
   } else {
     if (perm) return fail(RSA_ERR_UNSUPPORTED, "the permuted problem needs the tcgen05 kernel (bf16)");
+    if (!contiguous(g)) return fail(RSA_ERR_UNSUPPORTED, "strided q/k/v/out need the tcgen05 kernel");
     e = rsa::launch_attn_simt(g, q, k, v, out, lse, ws, rectify, false, st, &g_launches);
     if (e != cudaSuccess) return cuda_fail(e, "attn_simt(video)");
     if (text && g.Tt > 0) {
@@ -234,11 +280,8 @@ namespace {
 // K1; `reset_status` clears the device status flags first (a new call).  The
 // host-memory call keeps them across its head chunks, so an error raised by
 // any chunk survives to the final check.
-rsa_status pool_impl(const rsa_shape* shape, const void* q, const void* k, const void* v, void* workspace,
+rsa_status pool_geom(const rsa::Geometry& g, const void* q, const void* k, const void* v, void* workspace,
                      void* stream, bool reset_status) {
-  rsa::Geometry g;
-  rsa_status s = make_geometry(shape, &g);
-  if (s != RSA_OK) return s;
   if (!q || !k || !v || !workspace) return fail(RSA_ERR_SHAPE, "null pointer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   rsa::Workspace ws = bind(g, workspace);
@@ -249,8 +292,41 @@ rsa_status pool_impl(const rsa_shape* shape, const void* q, const void* k, const
   return RSA_OK;
 }
 
+rsa_status pool_impl(const rsa_shape* shape, const void* q, const void* k, const void* v, void* workspace,
+                     void* stream, bool reset_status) {
+  rsa::Geometry g;
+  rsa_status s = make_geometry(shape, &g);
+  if (s != RSA_OK) return s;
+  return pool_geom(g, q, k, v, workspace, stream, reset_status);
+}
+
+rsa_status select_geom(const rsa::Geometry& g, const rsa_config* cfg, void* workspace, void* stream) {
+  rsa_status s = check_config(cfg);
+  if (s != RSA_OK) return s;
+  if (!workspace) return fail(RSA_ERR_SHAPE, "null workspace");
+  // k_floor = math.ceil(top_k_fraction * M) (masks.py:100), IEEE double on the host
+  const int64_t k_floor = (int64_t)std::ceil(cfg->top_k_fraction * (double)g.M);
+  rsa::Workspace ws = bind(g, workspace);
+  cudaError_t e = rsa::launch_select(g, *cfg, k_floor, ws, static_cast<cudaStream_t>(stream), &g_launches);
+  if (e != cudaSuccess) return cuda_fail(e, "select");
+  return RSA_OK;
+}
+
+rsa_status attention_geom(const rsa_shape* shape, const rsa::Geometry& g, const rsa_config* cfg, const void* q,
+                          const void* k, const void* v, void* out, float* lse, void* workspace, void* stream) {
+  rsa_status s = check_config(cfg);
+  if (s != RSA_OK) return s;
+  if (!q || !k || !v || !out || !workspace) return fail(RSA_ERR_SHAPE, "null pointer");
+  rsa::Workspace ws = bind(g, workspace);
+  return run_attention(shape, g, ws, q, k, v, out, lse, rectifies(cfg->variant), true,
+                       static_cast<cudaStream_t>(stream));
+}
+
 rsa_status forward_impl(const rsa_shape* shape, const rsa_config* cfg, const void* q, const void* k,
                         const void* v, void* out, float* lse, void* workspace, void* stream, bool reset_status);
+rsa_status forward_geom(const rsa_shape* shape, const rsa::Geometry& g, const rsa_config* cfg, const void* q,
+                        const void* k, const void* v, void* out, float* lse, void* workspace, void* stream,
+                        bool reset_status);
 }  // namespace
 
 extern "C" {
@@ -264,15 +340,7 @@ rsa_status rsa_select(const rsa_shape* shape, const rsa_config* cfg, void* works
   rsa::Geometry g;
   rsa_status s = make_geometry(shape, &g);
   if (s != RSA_OK) return s;
-  s = check_config(cfg);
-  if (s != RSA_OK) return s;
-  if (!workspace) return fail(RSA_ERR_SHAPE, "null workspace");
-  // k_floor = math.ceil(top_k_fraction * M) (masks.py:100), IEEE double on the host
-  const int64_t k_floor = (int64_t)std::ceil(cfg->top_k_fraction * (double)g.M);
-  rsa::Workspace ws = bind(g, workspace);
-  cudaError_t e = rsa::launch_select(g, *cfg, k_floor, ws, static_cast<cudaStream_t>(stream), &g_launches);
-  if (e != cudaSuccess) return cuda_fail(e, "select");
-  return RSA_OK;
+  return select_geom(g, cfg, workspace, stream);
 }
 
 rsa_status rsa_attention(const rsa_shape* shape, const rsa_config* cfg, const void* q,
@@ -281,12 +349,7 @@ rsa_status rsa_attention(const rsa_shape* shape, const rsa_config* cfg, const vo
   rsa::Geometry g;
   rsa_status s = make_geometry(shape, &g);
   if (s != RSA_OK) return s;
-  s = check_config(cfg);
-  if (s != RSA_OK) return s;
-  if (!q || !k || !v || !out || !workspace) return fail(RSA_ERR_SHAPE, "null pointer");
-  rsa::Workspace ws = bind(g, workspace);
-  return run_attention(shape, g, ws, q, k, v, out, lse, rectifies(cfg->variant), true,
-                       static_cast<cudaStream_t>(stream));
+  return attention_geom(shape, g, cfg, q, k, v, out, lse, workspace, stream);
 }
 
 rsa_status rsa_forward(const rsa_shape* shape, const rsa_config* cfg, const void* q, const void* k,
@@ -295,16 +358,43 @@ rsa_status rsa_forward(const rsa_shape* shape, const rsa_config* cfg, const void
   return forward_impl(shape, cfg, q, k, v, out, lse, workspace, stream, true);
 }
 
+rsa_status rsa_forward_strided(const rsa_shape* shape, const rsa_config* cfg, const rsa_layout* layout,
+                               const rsa_layout* out_layout, const void* q, const void* k, const void* v,
+                               void* out, float* lse, void* workspace, void* stream) {
+  g_launches = 0;
+  rsa::Geometry g;
+  rsa_status s = make_geometry(shape, &g);
+  if (s != RSA_OK) return s;
+  const void* ptrs[4] = {q, k, v, out};
+  s = apply_layout(layout, out_layout, ptrs, 4, &g);
+  if (s != RSA_OK) return s;
+  if (!rsa::tc_supported(g) || shape->kernel == RSA_KERNEL_SIMT)
+    return fail(RSA_ERR_UNSUPPORTED, "strided q/k/v/out need the tcgen05 kernel (bf16, block and head_dim "
+                                     "in {64, 128})");
+  return forward_geom(shape, g, cfg, q, k, v, out, lse, workspace, stream, true);
+}
+
 }  // extern "C"
 
 namespace {
+rsa_status forward_geom(const rsa_shape* shape, const rsa::Geometry& g, const rsa_config* cfg, const void* q,
+                        const void* k, const void* v, void* out, float* lse, void* workspace, void* stream,
+                        bool reset_status) {
+  rsa_status s = check_config(cfg);
+  if (s != RSA_OK) return s;
+  s = pool_geom(g, q, k, v, workspace, stream, reset_status);
+  if (s != RSA_OK) return s;
+  s = select_geom(g, cfg, workspace, stream);
+  if (s != RSA_OK) return s;
+  return attention_geom(shape, g, cfg, q, k, v, out, lse, workspace, stream);
+}
+
 rsa_status forward_impl(const rsa_shape* shape, const rsa_config* cfg, const void* q, const void* k,
                         const void* v, void* out, float* lse, void* workspace, void* stream, bool reset_status) {
-  rsa_status s = pool_impl(shape, q, k, v, workspace, stream, reset_status);
+  rsa::Geometry g;
+  rsa_status s = make_geometry(shape, &g);
   if (s != RSA_OK) return s;
-  s = rsa_select(shape, cfg, workspace, stream);
-  if (s != RSA_OK) return s;
-  return rsa_attention(shape, cfg, q, k, v, out, lse, workspace, stream);
+  return forward_geom(shape, g, cfg, q, k, v, out, lse, workspace, stream, reset_status);
 }
 
 // per-thread pool of timing-free events for the host-memory call (no
@@ -434,6 +524,7 @@ rsa_status rsa_text_full_attention(int64_t heads, int64_t n_queries, int64_t n_k
   g.N = g.Tv / block; g.n_text = g.Tt > 0 ? 1 : 0; g.M = g.N + g.n_text;
   g.last_len = g.Tt; g.n_cols = 0; g.dtype = dtype; g.q_last = block;
   g.hb = heads; g.s_tok = head_dim; g.s_head = n_keys * head_dim; g.s_batch = heads * n_keys * head_dim;
+  g.o_hb = g.hb; g.o_tok = g.s_tok; g.o_head = g.s_head; g.o_batch = g.s_batch;
   g.qt_rows = n_queries; g.qt_row0 = 0; g.q_rows = n_queries;
   if (dtype < RSA_BF16 || dtype > RSA_F64) return fail(RSA_ERR_SHAPE, "bad dtype");
   if (head_dim < 1 || head_dim > (dtype == RSA_F64 ? 128 : 256))

@@ -108,7 +108,8 @@ pool_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restric
   const int64_t d = g.d;
   const int64_t row0 = kv_row0(g, blk);  // text blocks follow the video blocks contiguously
   const int64_t len = kv_len(g, blk);
-  const T* src = (seg == 0 ? q : seg == 1 ? k : v) + (h * g.T + row0) * d;
+  const T* src = (seg == 0 ? q : seg == 1 ? k : v) + row_off(g, h, row0);   // rows g.s_tok apart
+  const int64_t ts = g.s_tok;
 
   __shared__ double s_hi[2048];
 
@@ -142,7 +143,7 @@ pool_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restric
       for (; r + 7 * rg_count < len; r += 8 * rg_count) {
         float x[8][VEC];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) load_vec_f32<T, VEC>(src + (r + u * rg_count) * d + c * VEC, x[u]);
+        for (int u = 0; u < 8; ++u) load_vec_f32<T, VEC>(src + (r + u * rg_count) * ts + c * VEC, x[u]);
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
 #pragma unroll
@@ -161,7 +162,7 @@ pool_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restric
       }
       for (; r < len; r += rg_count) {
         float x[VEC];
-        load_vec_f32<T, VEC>(src + r * d + c * VEC, x);
+        load_vec_f32<T, VEC>(src + r * ts + c * VEC, x);
 #pragma unroll
         for (int i = 0; i < VEC; ++i) {
           acc[i] += (double)x[i];
@@ -202,7 +203,7 @@ pool_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restric
     // values and, for f64 data, copies the raw text keys)
     for (int64_t r = rg; r < len; r += rg_count) {
       double x[VEC];
-      load_vec<T, VEC>(src + r * d + c * VEC, x);
+      load_vec<T, VEC>(src + r * ts + c * VEC, x);
 #pragma unroll
       for (int i = 0; i < VEC; ++i) nonfinite |= !(fabs(x[i]) <= DBL_MAX);
       if (raw_out && !kTryPlain) {
@@ -222,7 +223,7 @@ pool_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restric
       for (int p = 0; p < rg_count; ++p) sum += s_hi[p * d + slot];
     } else {
       // correctly rounded (math.fsum) column sum, one thread per column
-      sum = fsum_exact(len, [&](int64_t r) { return to_f64(src[r * d + col]); });
+      sum = fsum_exact(len, [&](int64_t r) { return to_f64(src[r * ts + col]); });
     }
     const double flen = (double)len;
     const double mean = sum / flen;           // core.py:172 fsum(...) / length
@@ -539,7 +540,8 @@ cudaError_t launch_typed(const Geometry& g, const void* q, const void* k, const 
   dim3 grid((unsigned)g.M, 3, (unsigned)g.H);
   constexpr int V16 = 16 / sizeof(T);
   const bool aligned = (g.d % V16 == 0) && ((uintptr_t)q % 16 == 0) &&
-                       ((uintptr_t)k % 16 == 0) && ((uintptr_t)v % 16 == 0);
+                       ((uintptr_t)k % 16 == 0) && ((uintptr_t)v % 16 == 0) && g.s_tok % V16 == 0 &&
+                       g.s_head % V16 == 0 && g.s_batch % V16 == 0;
   if (aligned && g.d / V16 <= kThreads && (kThreads / (g.d / V16)) * g.d <= 2048) {
     pool_kernel<T, V16><<<grid, kThreads, 0, st>>>((const T*)q, (const T*)k, (const T*)v, ws, g);
   } else {

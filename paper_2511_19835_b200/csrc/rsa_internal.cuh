@@ -50,11 +50,18 @@ struct Geometry {
   // batch entry h / hb, head h % hb of it.  Contiguous [H][T][d]: hb = H,
   // s_tok = d, s_head = T d, s_batch = H T d (rsa_shape without a layout).
   int64_t hb, s_tok, s_head, s_batch;
+  // the same for the output O (a strided call may write a layout of its own)
+  int64_t o_hb, o_tok, o_head, o_batch;
 };
 
 // element offset of row `row` of head h
 __host__ __device__ __forceinline__ int64_t row_off(const Geometry& g, int64_t h, int64_t row) {
   return (h / g.hb) * g.s_batch + (h % g.hb) * g.s_head + row * g.s_tok;
+}
+
+// element offset of output row `row` of head h
+__host__ __device__ __forceinline__ int64_t out_off(const Geometry& g, int64_t h, int64_t row) {
+  return (h / g.o_hb) * g.o_batch + (h % g.o_hb) * g.o_head + row * g.o_tok;
 }
 
 // tokens in video (query) block n

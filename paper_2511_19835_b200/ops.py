@@ -26,10 +26,19 @@ def rectified_sparse_attention_op(q: torch.Tensor, k: torch.Tensor, v: torch.Ten
                  variant=variant)
 
 
+def _out_like(q, k, v):
+    """The real op's output layout: dense in q's dimension order when q/k/v go
+    down the strided (no-copy) path, else contiguous."""
+    from .pipeline import _dense_like
+    strided = (not (q.is_contiguous() and k.is_contiguous() and v.is_contiguous()) and q.dtype == torch.bfloat16
+               and q.dim() <= 4 and q.stride() == k.stride() == v.stride() and q.stride(-1) == 1)
+    return _dense_like(q) if strided else q.new_empty(q.shape)
+
+
 @rectified_sparse_attention_op.register_fake
 def _(q, k, v, num_text_tokens, block, top_k_fraction, weight_threshold, adjacency_radius,
       force_text_blocks, variant):
-    return torch.empty_like(q)
+    return _out_like(q, k, v)
 
 
 @torch.library.custom_op(f"{_LIB_NS}::rectified_sparse_attention_status", mutates_args=())
@@ -52,4 +61,4 @@ def rectified_sparse_attention_status_op(q: torch.Tensor, k: torch.Tensor, v: to
 @rectified_sparse_attention_status_op.register_fake
 def _(q, k, v, num_text_tokens, block, top_k_fraction, weight_threshold, adjacency_radius,
       force_text_blocks, variant):
-    return torch.empty_like(q), q.new_empty(4, dtype=torch.int32)
+    return _out_like(q, k, v), q.new_empty(4, dtype=torch.int32)

@@ -324,10 +324,26 @@ def rectified_sparse_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor
         if k.is_cuda or v.is_cuda:
             raise ShapeError("q, k and v must all be host tensors or all CUDA tensors")
         return _forward_from_host(q, k, v, shape, cfg, lse, workspace, heads_per_chunk, status)
-    q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+    strided = _strided_layout(q, k, v, kernel, morton)
+    if strided is None:
+        q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
     workspace = _checked_workspace(workspace, shape, q.device)
     _check_lse(lse, heads * T, q.device)
-    if morton:
+    if strided is not None:
+        # row-contiguous views ([B, T, H, d] transposed to [B, H, T, d], head
+        # slices of a fused qkv buffer, ...) go straight to the kernels through
+        # their strides: no copy.  The output keeps q's dimension order (dense).
+        if out is None:
+            out = _dense_like(q)
+        if out.shape != q.shape or out.dtype != q.dtype or out.device != q.device:
+            raise ShapeError(f"out must be a {q.dtype} tensor of shape {tuple(q.shape)} on {q.device}")
+        out_layout = _layout_of(out)
+        if out_layout is None:
+            raise ShapeError("out must have rows of d contiguous elements at 16-byte aligned strides")
+        nat.check(nat.lib().rsa_forward_strided(C.byref(shape), C.byref(cfg), C.byref(strided), C.byref(out_layout),
+                                                _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), _ptr(workspace),
+                                                _stream()))
+    elif morton:
         from .errors import MissingGridError
         from .reorder import device_permutation, permuted_forward
         if grid_dims is None:
@@ -347,6 +363,50 @@ def rectified_sparse_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor
                                         _ptr(out), _ptr(lse), _ptr(workspace), _stream()))
     _report_status(workspace, status, check_status)
     return out
+
+
+def _layout_of(x: torch.Tensor):
+    """rsa_layout of a [..., T, d] view (up to 4-D) whose rows are contiguous
+    and whose token / head / batch strides are multiples of 8 elements (16-byte
+    TMA rows), else None."""
+    if x.dim() > 4 or x.stride(-1) != 1 or x.data_ptr() % 16:
+        return None
+    st, shp = list(x.stride()), list(x.shape)
+    while len(shp) < 4:
+        shp.insert(0, 1)
+        st.insert(0, 0)
+    B, H, T = shp[0], shp[1], shp[2]
+    # (a size-1 dimension's stride is never used: give it a dense value)
+    tok = st[2]
+    head = st[1] if H > 1 else tok * T
+    bat = st[0] if B > 1 else head * H
+    if tok % 8 or head % 8 or bat % 8:
+        return None
+    return nat.TensorLayout(int(H), int(tok), int(head), int(bat))
+
+
+def _strided_layout(q, k, v, kernel, morton):
+    """An rsa_layout for non-contiguous bf16 CUDA q/k/v of one shared stride
+    pattern with contiguous rows -- e.g. the model's [B, T, H, d] projection
+    output viewed as [B, H, T, d].  None: the contiguous path (copying if
+    needed)."""
+    if q.is_contiguous() and k.is_contiguous() and v.is_contiguous():
+        return None
+    if morton or kernel == "simt" or q.dtype != torch.bfloat16 or not (q.stride() == k.stride() == v.stride()):
+        return None
+    if any(x.data_ptr() % 16 for x in (k, v)):
+        return None
+    return _layout_of(q)
+
+
+def _dense_like(x: torch.Tensor) -> torch.Tensor:
+    """A dense tensor of x's shape whose dimensions are laid out in x's stride
+    order (empty_like does that only for dense x): the output of a
+    [B, T, 3, H, d] fused-qkv slice is a dense [B, T, H, d] buffer."""
+    order = sorted(range(x.dim()), key=lambda i: (-x.stride(i), i))
+    buf = torch.empty([x.shape[i] for i in order], dtype=x.dtype, device=x.device)
+    inv = [order.index(i) for i in range(x.dim())]
+    return buf.permute(inv)
 
 
 def _report_status(workspace: torch.Tensor, status: torch.Tensor | None, check: bool) -> None:

@@ -134,6 +134,26 @@ def test_torch_library_op():
     assert_bf16_close(out[0], np.concatenate([ref["o_video"], ref["o_text"]]), "torch.ops")
 
 
+def test_torch_library_opcheck_and_compile():
+    """torch.library.opcheck (schema, fake/meta kernel vs the CUDA kernel,
+    AOT dispatch) on the registered op, contiguous and strided inputs, and a
+    torch.compile(fullgraph=True) graph that calls it."""
+    from paper_2511_19835_b200 import ops  # noqa: F401
+    op = torch.ops.rsa_b200.rectified_sparse_attention.default
+    g = torch.Generator().manual_seed(3)
+    x = [torch.randn(1, 64 * 12 + 40, 2, 64, generator=g).to(torch.bfloat16).cuda() for _ in range(3)]
+    args = (40, 64, 0.3, 0.2, 1, True, "sparse-rectified")
+    for q, k, v in (tuple(t.transpose(1, 2).contiguous() for t in x), tuple(t.transpose(1, 2) for t in x)):
+        torch.library.opcheck(op, (q, k, v) + args)
+
+    def f(q, k, v):
+        return torch.ops.rsa_b200.rectified_sparse_attention(q, k, v, *args) * 0.5
+
+    q, k, v = (t.transpose(1, 2) for t in x)
+    compiled = torch.compile(f, fullgraph=True, backend="aot_eager")
+    assert torch.equal(compiled(q, k, v), f(q, k, v))
+
+
 def test_determinism_bitwise():
     qv, qt, k, v = cfg1_inputs(43)
     prob = bf16_problem(qv, qt, k, v, 64)
