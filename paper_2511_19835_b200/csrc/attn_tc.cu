@@ -29,6 +29,8 @@ namespace {
 constexpr int kThreads = 384;   // 4 control warps + 8 softmax warps
 constexpr float kRescaleThreshold = 12.0f;  // log2 units: rescale O only if the row max grows by > 2^12
                                             // (P <= 2^12 stays exact-range in bf16 / fp32; 8 measured ~1 % slower)
+constexpr float kSpecSum = 8192.0f;         // paired-tile kernel: keep the running base while a block's row
+                                            // sum of P stays <= 2^13 (so does every P)
 
 // persistent kernel: Q resident in TMEM (A operand of the S MMAs), two S/P
 // TMEM buffers, a K/V ring of NST stages in shared memory
@@ -1366,27 +1368,27 @@ attn_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         if (wtid == 0) PAIR_TRACE(1 + t, tr + 2, clock64());
         if (len == 128 && __all_sync(0xffffffffu, m_run != -INFINITY)) {
           // Speculative: exponentiate against the running base m_run while the
-          // block max is still being found, and the second half of S is still
-          // loading.  The lazy-rescale rule keeps m_run unless the block max
-          // exceeds it by more than 2^kRescaleThreshold -- then (rarely, and
-          // warp-wide because tcgen05.st is warp-collective) redo all four
-          // chunks against the new base.  Same decisions and bases as the
-          // max-first path, so the same P bits.
+          // second half of S is still loading, with no row max on the critical
+          // path.  The base is kept while this block's P stays bounded: a row
+          // sum <= 2^kSpecSumLog2 implies every P <= 2^kSpecSumLog2 (fine for
+          // bf16 P and fp32 O / l).  Otherwise (rarely; warp-wide, because
+          // tcgen05.st is warp-collective) the block is redone against its true
+          // row max, as the max-first path would -- any base gives the same
+          // softmax, the choice only moves rounding.
           ptx::tmem_ld32(s_addr + 64, sr[2]);
           ptx::tmem_ld32(s_addr + 96, sr[3]);
           const float2 nb2 = make_float2(-m_run, -m_run);
           if (wtid == 0) PAIR_TRACE(1 + t, tr + 3, clock64());
           exp_chunk(0, nb2);
           exp_chunk(1, nb2);
-          float mx = max2(0, -INFINITY);
           ptx::tmem_ld_wait();
           exp_chunk(2, nb2);
           exp_chunk(3, nb2);
-          mx = max2(2, mx);
-          const float m_blk = mx * sl2;
-          const bool redo = m_blk > m_run + kRescaleThreshold;
+          const float2 ps = ptx::fadd2(sum2[0], sum2[1]);
+          const bool redo = !(ps.x + ps.y <= kSpecSum);   // (NaN-safe)
           if (__any_sync(0xffffffffu, redo)) {
             if (redo) {
+              const float m_blk = max2(2, max2(0, -INFINITY)) * sl2;
               alpha = ptx::ex2(m_run - m_blk);
               rescale_o = true;
               m_run = m_blk;
