@@ -17,9 +17,9 @@ timeout -s KILL 900 python bench.py --impl reference --steps 3 --warmup 1 > "$O/
 timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file "$O/launches.csv" python bench.py --profile --steps 2 --warmup 3 > "$O/ncu_launches.log" 2>&1
 # full captures: K3 (one launch), K1, K2
-timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:attn_tc -s 3 -c 1 \
+timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:attn_tc_pair -s 3 -c 1 \
   -o "$O/k3" python bench.py --profile --steps 1 --warmup 3 > "$O/ncu_k3.log" 2>&1
-timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:"pool_bulk|select_rows|dgemm|text_combine|tile_lists" -s 5 -c 5 \
+timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:"pool_warp|select_rows|dgemm|text_combine" -s 4 -c 4 \
   -o "$O/k12" python bench.py --profile --steps 1 --warmup 3 > "$O/ncu_k12.log" 2>&1
 ls -la "$O"
 for f in pytest_gpu smoke; do tail -n 2 "$O/$f.log"; done; for f in bench_hv bench_wan bench_ref; do tail -n 1 "$O/$f.log"; done
