@@ -3,9 +3,9 @@ HunyuanVideo 720p (T_v 118,784, T_t 256, d = B = 128) and Wan 2.1 (T_v 75,520,
 T_t 0), 90 % sparsity, through the batched op a model calls.
 
 The call carries every head of the real configuration (24 / 40), so the
-default tcgen05 kernel runs in its steady state: ~75 query tiles per
-ping-pong slot, crossing head boundaries (the scheduling regime the bench
-measures).  Heads alternate between two seeded problems, which gives three
+default tcgen05 kernel (the paired-tile K3) runs in its steady state: ~76
+query-tile pairs per CTA, crossing head boundaries (the scheduling regime
+the bench measures).  Heads alternate between two seeded problems, which gives three
 independent checks:
 
   * sampled rows against the REFERENCE's own outputs on the same bf16-valued
