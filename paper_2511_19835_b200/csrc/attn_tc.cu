@@ -1362,8 +1362,9 @@ attn_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         };
         float alpha = 1.f;
         bool rescale_o = false;
+        // TMEM -> registers runs at ~64 B/clk per SMSP (16 KB per block per
+        // warp): only the first 32 columns are waited for before the exps start
         ptx::tmem_ld32(s_addr, sr[0]);
-        ptx::tmem_ld32(s_addr + 32, sr[1]);
         ptx::tmem_ld_wait();
         if (wtid == 0) PAIR_TRACE(1 + t, tr + 2, clock64());
         if (len == 128 && __all_sync(0xffffffffu, m_run != -INFINITY)) {
@@ -1375,13 +1376,14 @@ attn_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
           // tcgen05.st is warp-collective) the block is redone against its true
           // row max, as the max-first path would -- any base gives the same
           // softmax, the choice only moves rounding.
+          ptx::tmem_ld32(s_addr + 32, sr[1]);
           ptx::tmem_ld32(s_addr + 64, sr[2]);
           ptx::tmem_ld32(s_addr + 96, sr[3]);
           const float2 nb2 = make_float2(-m_run, -m_run);
           if (wtid == 0) PAIR_TRACE(1 + t, tr + 3, clock64());
           exp_chunk(0, nb2);
-          exp_chunk(1, nb2);
           ptx::tmem_ld_wait();
+          exp_chunk(1, nb2);
           exp_chunk(2, nb2);
           exp_chunk(3, nb2);
           const float2 ps = ptx::fadd2(sum2[0], sum2[1]);
@@ -1401,6 +1403,7 @@ attn_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
           }
         } else {
           // first block of the tile (or a ragged block): row max first
+          ptx::tmem_ld32(s_addr + 32, sr[1]);
           ptx::tmem_ld32(s_addr + 64, sr[2]);
           ptx::tmem_ld32(s_addr + 96, sr[3]);
           ptx::tmem_ld_wait();
