@@ -72,7 +72,8 @@ def parse():
     ap.add_argument("--weight-threshold", type=float, default=0.0,
                     help="cumulative-weight rule p (masks.py:99-103); the headline config uses 0")
     ap.add_argument("--variant", default="sparse-rectified")
-    ap.add_argument("--kernel", default="auto", choices=["auto", "tcgen05", "simt"])
+    ap.add_argument("--kernel", default="auto",
+                    choices=["auto", "tcgen05", "simt", "tcgen05-pingpong", "tcgen05-persistent"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-chunk", type=int, default=1, help="heads per pipelined chunk of the e2e call")
     ap.add_argument("--no-cpu-baseline", action="store_true")

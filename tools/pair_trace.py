@@ -21,9 +21,11 @@ from paper_2511_19835_b200.pipeline import _ptr, _stream, workspace_for  # noqa:
 
 cfg = bench.CONFIGS["hv"]
 dev = torch.device("cuda", 0)
-heads = int(sys.argv[1]) if len(sys.argv) > 1 else 24
+heads = 24
+kernel = sys.argv[1] if len(sys.argv) > 1 else "tcgen05"   # "tcgen05-pingpong": the two-slot kernel
+pp = kernel == "tcgen05-pingpong"
 q, k, v = bench.synth_inputs(torch, cfg, heads, 1234, dev)
-shape = nat.make_shape(heads, cfg["t_v"], cfg["t_t"], 128, 128, "bfloat16", "tcgen05")
+shape = nat.make_shape(heads, cfg["t_v"], cfg["t_t"], 128, 128, "bfloat16", kernel)
 conf = nat.make_config(0.1, 0.0, 0, False, "sparse-rectified")
 ws = workspace_for(shape, dev)
 out = torch.empty_like(q)
@@ -43,9 +45,9 @@ pw = mma[1:n:3]
 go = mma[2:n:3]
 ok = req > 0
 req, kind, pw, go = req[ok], kind[ok], pw[ok], go[ok]
-names = ["S0", "PV1", "S1", "PV0"]
+names = ["S", "PV", "-", "-"] if pp else ["S0", "PV1", "S1", "PV0"]
 print(f"MMA groups traced: {len(req)}")
-for q4 in range(4):
+for q4 in range(2 if pp else 4):
     sel = kind == q4
     w = (go - req)[sel]
     line = f"  {names[q4]:4s} wait before issue: median {np.median(w):6.0f} mean {w.mean():6.0f}"
@@ -55,7 +57,8 @@ for q4 in range(4):
     print(line)
 s0 = np.nonzero(kind == 0)[0]
 per = np.diff(req[s0])
-print(f"  iteration period (S0 to S0): median {np.median(per):.0f}  mean {per.mean():.0f} cycles")
+print(f"  {'S-group period (one 64-key half of slot 0)' if pp else 'iteration period (S0 to S0)'}: "
+      f"median {np.median(per):.0f}  mean {per.mean():.0f} cycles")
 issue = np.diff(np.append(go, go[-1]))  # go -> next req
 gi = req[1:] - go[:-1]
 print(f"  issue time of a group (go -> next request): median {np.median(gi):.0f}")
@@ -85,7 +88,7 @@ i0 = s0[len(s0) // 2]
 t0 = req[i0]
 print("excerpt (cycles relative to an S0 request): kind req [P ok] go")
 for i in range(i0, min(i0 + 8, len(req))):
-    print(f"  {names[kind[i]]:4s} {req[i] - t0:8d} {(pw[i] - t0) if kind[i] % 2 else '':>8} {go[i] - t0:8d}")
+    print(f"  {names[kind[i]]:4s} {req[i] - t0:8d} {(pw[i] - t0) if kind[i] % 2 and pw[i] else '':>8} {go[i] - t0:8d}")
 for t in range(2):
     x = tr[1 + t]
     b = x[1::6]; c = x[5::6]
