@@ -1223,11 +1223,12 @@ attn_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
       // a tile with an empty kv list (the C ABI's mask seam flags it as
       // RSA_ERR_EMPTY_ROW): its group still loaded Q and releases one P phase
       // after its previous epilogue; answer with the o_full phase (so o_full
-      // can never run a phase ahead of the group)
+      // can never run a phase ahead of the group).  Its Q phase is skipped, not
+      // waited for: the group may already have started the next tile's Q load
+      // on the same barrier (a parity wait here would alias that phase).
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
         if ((t == 0 ? c0 : c1) == 0 && (t == 0 || e1)) {
-          ptx::mbar_wait(q_full + t, (qbits >> t) & 1u);
           qbits ^= 1u << t;
           ptx::mbar_wait(p_full + t, (pbits >> t) & 1u);
           pbits ^= 1u << t;

@@ -76,24 +76,40 @@ def test_torch_op_status_output():
         torch.ops.rsa_b200.rectified_sparse_attention(q, k, v, 30, 64, 0.1, 0.0, 0, False, "sparse-rectified")
 
 
-@pytest.mark.timeout(120)
-def test_empty_mask_row_on_pingpong_kernel_returns_status_not_hang():
+@pytest.mark.timeout(180)
+@pytest.mark.parametrize("kernel", ["tcgen05", "tcgen05-pingpong", "tcgen05-persistent"])
+def test_empty_mask_rows_return_status_not_hang(kernel):
     """a video tile with an empty kv list issued no S MMA, so the
     ping-pong producer waited forever for its Q buffer.  The C ABI seam must
-    return RSA_ERR_EMPTY_ROW (d = B = 128, bf16: the ping-pong kernel)."""
-    heads, t_v, t_t, d, b = 1, 128 * 6, 0, 128, 128
+    return RSA_ERR_EMPTY_ROW on every d = B = 128 tcgen05 kernel -- with empty
+    tiles in either slot of a pair, both slots of one pair, and CTAs that run
+    further tiles after an empty one (64 heads: ~2 tile pairs per CTA) -- and
+    the non-empty rows must equal the all-rows-retained call's rows."""
+    heads, t_v, t_t, d, b = 64, 128 * 6, 0, 128, 128
     q, k, v = (x[0] for x in qkv(heads, t_v, t_t, d))
-    shape = nat.make_shape(heads, t_v, t_t, d, b, "bfloat16", "tcgen05")
+    shape = nat.make_shape(heads, t_v, t_t, d, b, "bfloat16", kernel)
     ws = workspace_for(shape, q.device)
-    mask = torch.ones(6, 6, dtype=torch.uint8, device="cuda")
-    mask[3] = 0
-    out = torch.zeros_like(q)
-    lse = torch.empty(t_v + t_t, dtype=torch.float32, device="cuda")
-    nat.check(nat.lib().rsa_block_sparse_attention(C.byref(shape), _ptr(q), _ptr(k), _ptr(v), _ptr(mask),
-                                                   _ptr(out), _ptr(lse), _ptr(ws), _stream()))
-    assert nat.lib().rsa_check_device_status(_ptr(ws), _stream()) == 3   # RSA_ERR_EMPTY_ROW
+    full = torch.ones(heads, 6, 6, dtype=torch.uint8, device="cuda")
+    mask = full.clone()
+    mask[0, 3] = 0            # slot 1 of a pair
+    mask[0, 4] = mask[0, 5] = 0   # both slots of a pair
+    mask[7, 0] = 0            # slot 0
+    mask[40, 2] = 0
+    lse = torch.empty(heads * (t_v + t_t), dtype=torch.float32, device="cuda")
+
+    def run(m):
+        out = torch.zeros_like(q)
+        nat.check(nat.lib().rsa_block_sparse_attention(C.byref(shape), _ptr(q), _ptr(k), _ptr(v), _ptr(m),
+                                                       _ptr(out), _ptr(lse), _ptr(ws), _stream()))
+        return out, nat.lib().rsa_check_device_status(_ptr(ws), _stream())
+
+    out, status = run(mask)
+    assert status == 3   # RSA_ERR_EMPTY_ROW
+    ref, status_ref = run(full)
+    assert status_ref == 0
     torch.cuda.synchronize()
-    assert torch.isfinite(out[:3 * 128].float()).all()
+    keep = mask.bool().any(-1).repeat_interleave(b, dim=1)            # [heads, t_v] rows with a kv block
+    assert torch.equal(out[keep], ref[keep])
 
 
 def test_morton_check_status_without_workspace():
