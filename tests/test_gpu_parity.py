@@ -511,14 +511,16 @@ def test_non_finite_inputs_raise_shape_error(dtype, where):
                                            sparsity=0.5, check_status=True)
 
 
-@pytest.mark.parametrize("heads", [1, 12])
+@pytest.mark.parametrize("heads", [1, 15])
 def test_pair_pingpong_and_persistent_k3_agree(heads):
     """d = B = 128 runs the paired-tile K3 by default; kernel="tcgen05-pingpong"
     and "tcgen05-persistent" select the two-slot ping-pong and the one-tile
     persistent K3 (cross-checks, never chosen silently): all within the bf16
-    bar of each other and of the oracle.  12 heads put ~2 tile pairs on every
-    CTA (pairs straddle heads and the text/video boundary)."""
-    qv, qt, k, v = (O.round_to_bf16(x) for x in O.gen_synthetic(5, 128 * 20, 200, 128, 128, (1, 40, 64), 1.0, 2.0, 0.3))
+    bar of each other and of the oracle.  23 tiles per head (2 text + 21
+    video): an odd tile count (the last pair has one tile), and at 15 heads
+    (345 tiles) CTAs run two pairs that straddle heads and the text/video
+    boundary."""
+    qv, qt, k, v = (O.round_to_bf16(x) for x in O.gen_synthetic(5, 128 * 21, 200, 128, 128, (1, 42, 64), 1.0, 2.0, 0.3))
     q = torch.cat([to_bf16_tensor(qv), to_bf16_tensor(qt)])[None].expand(heads, -1, -1).contiguous()
     kk = to_bf16_tensor(k)[None].expand(heads, -1, -1).contiguous()
     vv = to_bf16_tensor(v)[None].expand(heads, -1, -1).contiguous()
