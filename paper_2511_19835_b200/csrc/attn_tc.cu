@@ -1005,7 +1005,10 @@ __device__ long long g_pair_trace[4][16384];
 
 struct CfgPair {
   static constexpr int D = 128, BKV = 128;
-  static constexpr int NST = 5;                    // K/V ring stages
+#ifndef RSA_PAIR_NST
+#define RSA_PAIR_NST 5
+#endif
+  static constexpr int NST = RSA_PAIR_NST;         // K/V ring stages
   static constexpr int STAGE = BKV * D * 2;        // 32 KB
   static constexpr int PANEL = 128 * 128;          // 16 KB: 128 rows x 128 B (64 columns)
   static constexpr int Q_BYTES = 128 * D * 2;      // 32 KB
@@ -1017,6 +1020,9 @@ struct CfgPair {
 };
 #ifndef RSA_PAIR_POLY
 #define RSA_PAIR_POLY 0   // column pairs per 32-column chunk whose 2^x runs on the FMA pipe
+#endif
+#ifndef RSA_PAIR_KV_HINT
+#define RSA_PAIR_KV_HINT 0   // A/B: 1 = K/V loads without the evict_last L2 hint
 #endif
 #ifndef RSA_PAIR_L2PF
 #define RSA_PAIR_L2PF 0   // iterations ahead whose K/V blocks the producer prefetches into L2 (0: off)
@@ -1071,7 +1077,11 @@ attn_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     // ===================== TMA producer: K/V blocks in MMA order =====================
       ptx::prefetch_tmap(&tm_k);
       ptx::prefetch_tmap(&tm_v);
+#if RSA_PAIR_KV_HINT == 1
+      const uint64_t keep = ptx::policy_evict_normal();
+#else
       const uint64_t keep = ptx::policy_evict_last();   // K/V blocks are re-read by many tiles of the head
+#endif
       int st = 0;
       uint32_t ph = 0;
       int ptr = 0;   // trace index (RSA_PAIR_TRACE)
