@@ -1021,6 +1021,10 @@ struct CfgPair {
 #ifndef RSA_PAIR_POLY
 #define RSA_PAIR_POLY 0   // column pairs per 32-column chunk whose 2^x runs on the FMA pipe
 #endif
+#ifndef RSA_PAIR_SPIN
+#define RSA_PAIR_SPIN 1   // poll (test_wait) instead of try_wait: 1 the MMA thread's P waits (A/B over four
+                          // rounds: -1.9 % K3), 2 the softmax S waits (no gain)
+#endif
 #ifndef RSA_PAIR_KV_HINT
 #define RSA_PAIR_KV_HINT 0   // A/B: 1 = K/V loads without the evict_last L2 hint
 #endif
@@ -1197,7 +1201,11 @@ attn_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     };
     auto issue_pv = [&](int t, bool first, bool last) {
       PAIR_TRACE(0, tr, (clock64() << 2) | (t ? 1 : 3));
+#if RSA_PAIR_SPIN & 1
+      ptx::mbar_spin(p_full + t, (pbits >> t) & 1u);
+#else
       ptx::mbar_wait(p_full + t, (pbits >> t) & 1u);   // P_t_j written, V_t_j (and K_t_{j+1}) landed
+#endif
       pbits ^= 1u << t;
       ptx::tc_fence_after();
       PAIR_TRACE(0, tr + 1, clock64());
@@ -1341,7 +1349,11 @@ attn_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         if (list && j + 1 < count) ent_next = list[j + 1];
         const int len = (int)kv_len(g, m);
         if (wtid == 0) PAIR_TRACE(1 + t, tr, clock64());
+#if RSA_PAIR_SPIN & 2
+        ptx::mbar_spin(s_full + t, ns & 1u);
+#else
         ptx::mbar_wait(s_full + t, ns & 1u);
+#endif
         ++ns;
         ptx::tc_fence_after();
         if (wtid == 0) PAIR_TRACE(1 + t, tr + 1, clock64());

@@ -56,10 +56,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   } while (!done);
 }
 
-// spin on the phase without the try_wait suspend (lowest wake-up latency)
+// spin on the phase without the try_wait suspend (lowest wake-up latency),
+// with the same deadlock watchdog as mbar_wait
 __device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   uint32_t done = 0;
+  long long t0 = 0;
+  uint32_t spins = 0;
   do {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -68,6 +71,16 @@ __device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t parity) {
         : "=r"(done)
         : "r"(addr), "r"(parity)
         : "memory");
+    if (!done && ((++spins & 0xFFFFu) == 0)) {
+      const long long now = clock64();
+      if (t0 == 0) {
+        t0 = now;
+      } else if (now - t0 > (1ll << 32)) {
+        printf("rsa_b200: mbarrier spin timeout (smem 0x%x parity %u) block %d thread %d\n", addr, parity,
+               (int)blockIdx.x, (int)threadIdx.x);
+        __trap();
+      }
+    }
   } while (!done);
 }
 
