@@ -88,6 +88,9 @@ rsa_status check_layout(const rsa_layout* l, const rsa::Geometry& g) {
     return fail(RSA_ERR_SHAPE, "layout strides must be non-negative and token_stride >= head_dim");
   if (l->token_stride % 8 || l->head_stride % 8 || l->batch_stride % 8)
     return fail(RSA_ERR_UNSUPPORTED, "layout strides must be multiples of 8 elements (16-byte TMA rows)");
+  // (an expanded / broadcast dimension -- stride 0 -- is not a TMA-mappable view)
+  if ((l->heads_per_batch > 1 && l->head_stride == 0) || (g.H / l->heads_per_batch > 1 && l->batch_stride == 0))
+    return fail(RSA_ERR_UNSUPPORTED, "layout strides of dimensions longer than 1 must be non-zero");
   return RSA_OK;
 }
 

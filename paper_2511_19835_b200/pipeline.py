@@ -380,7 +380,7 @@ def _layout_of(x: torch.Tensor):
     tok = st[2]
     head = st[1] if H > 1 else tok * T
     bat = st[0] if B > 1 else head * H
-    if tok % 8 or head % 8 or bat % 8:
+    if tok % 8 or head % 8 or bat % 8 or head == 0 or bat == 0:   # (broadcast dims: copy instead)
         return None
     return nat.TensorLayout(int(H), int(tok), int(head), int(bat))
 

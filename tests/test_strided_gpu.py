@@ -68,6 +68,18 @@ def test_fused_qkv_slices_equal_contiguous_bitwise():
     assert torch.equal(out, want)
 
 
+def test_broadcast_kv_views_fall_back_to_copies():
+    """k/v expanded over heads (stride 0, GQA-style) are not TMA-mappable views:
+    the op copies them and still matches the materialised call."""
+    B, H, T, d = 1, 3, 128 * 8 + 64, 128
+    q = torch.randn(B, H, T, d).to(torch.bfloat16).cuda()
+    k1, v1 = (torch.randn(B, 1, T, d).to(torch.bfloat16).cuda() for _ in range(2))
+    k, v = k1.expand(B, H, T, d), v1.expand(B, H, T, d)
+    kw = dict(num_text_tokens=64, block=128, top_k_fraction=0.3)
+    want = rsa.rectified_sparse_attention(q, k.contiguous(), v.contiguous(), **kw)
+    assert torch.equal(rsa.rectified_sparse_attention(q, k, v, **kw), want)
+
+
 def test_strided_c_abi_rejects_unsupported_layouts():
     shape = nat.make_shape(2, 128 * 4, 0, 128, 128, "bfloat16")
     cfg = nat.make_config(0.5, 0.0, 0, False, "sparse-rectified")
@@ -82,3 +94,6 @@ def test_strided_c_abi_rejects_unsupported_layouts():
     ok = nat.TensorLayout(2, 128, 128 * 4 * 128, 0)
     with pytest.raises(NativeError):                              # strided views are a bf16 / tcgen05 path
         nat.check(nat.lib().rsa_forward_strided(fp, cfg, ok, None, p(y), p(y), p(y), p(y), None, p(ws), None))
+    bcast = nat.TensorLayout(2, 128, 0, 0)                         # a broadcast head dimension
+    with pytest.raises(NativeError):
+        nat.check(nat.lib().rsa_forward_strided(shape, cfg, bcast, None, p(x), p(x), p(x), p(x), None, p(ws), None))
