@@ -1,64 +1,72 @@
-"""torch.library registration of the hot path as ``torch.ops.rsa_b200.*``.
+"""``torch.ops.rsa_b200.*``: the hot path as registered PyTorch operators.
 
-The ops call straight into the C ABI (include/rsa_b200.h) on the current
-stream; fake (meta) kernels describe output shapes so the op composes with
-tracing.  A model integration replaces its attention call with
-``torch.ops.rsa_b200.rectified_sparse_attention(q, k, v, num_text, block, ...)``.
+The registration is C++ (``csrc/torch_ops.cpp``, ``TORCH_LIBRARY(rsa_b200)``,
+built into ``librsa_b200_torch.so`` over the C ABI of ``librsa_b200.so``),
+with CUDA and Meta kernels, so the ops trace under ``torch.compile`` and pass
+``torch.library.opcheck``.  Importing this module loads that library; without
+it the import raises NativeError (no Python fallback).
+
+    torch.ops.rsa_b200.rectified_sparse_attention(q, k, v, num_text_tokens, block=128,
+        top_k_fraction=0.1, weight_threshold=0.0, adjacency_radius=0,
+        force_text_blocks=False, variant="sparse-rectified") -> Tensor
+    torch.ops.rsa_b200.rectified_sparse_attention_status(...) -> (Tensor, Tensor int32[4])
+
+q/k/v are ``[..., T, d]`` (the last ``num_text_tokens`` rows text; reference
+core.py:6-8), config as SparsityConfig (masks.py:30-33), variant as VARIANTS
+(rectify.py:23-24).  The first op checks the device flags eagerly (one stream
+sync, like the reference's eager checks); the second returns them for
+``raise_for_status``.  Operator errors surface as RuntimeError whose message
+starts with the reference exception's class name; :func:`rectified_sparse_attention`
+here re-raises them as those classes (errors.py:4-45).
 """
 
 from __future__ import annotations
 
+import os
+from pathlib import Path
+
 import torch
 
-from .pipeline import rectified_sparse_attention as _impl
+from . import errors
+from ._native import lib as _load_native
+from .errors import NativeError
 
-_LIB_NS = "rsa_b200"
-
-
-@torch.library.custom_op(f"{_LIB_NS}::rectified_sparse_attention", mutates_args=())
-def rectified_sparse_attention_op(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
-                                  num_text_tokens: int, block: int, top_k_fraction: float,
-                                  weight_threshold: float, adjacency_radius: int,
-                                  force_text_blocks: bool, variant: str) -> torch.Tensor:
-    return _impl(q, k, v, num_text_tokens=num_text_tokens, block=block,
-                 top_k_fraction=top_k_fraction, weight_threshold=weight_threshold,
-                 adjacency_radius=adjacency_radius, force_text_blocks=force_text_blocks,
-                 variant=variant)
+TORCH_LIB_PATH = Path(os.environ.get("RSA_B200_TORCH_LIB",
+                                     Path(__file__).resolve().parent / "librsa_b200_torch.so"))
 
 
-def _out_like(q, k, v):
-    """The real op's output layout: dense in q's dimension order when q/k/v go
-    down the strided (no-copy) path, else contiguous."""
-    from .pipeline import _dense_like
-    strided = (not (q.is_contiguous() and k.is_contiguous() and v.is_contiguous()) and q.dtype == torch.bfloat16
-               and q.dim() <= 4 and q.stride() == k.stride() == v.stride() and q.stride(-1) == 1)
-    return _dense_like(q) if strided else q.new_empty(q.shape)
+def _load() -> None:
+    if hasattr(torch.ops.rsa_b200, "rectified_sparse_attention"):
+        return
+    _load_native()    # the C ABI library it links against (raises if missing)
+    if not TORCH_LIB_PATH.exists():
+        raise NativeError(f"{TORCH_LIB_PATH} is missing: run `python -m paper_2511_19835_b200.build`")
+    torch.ops.load_library(str(TORCH_LIB_PATH))
 
 
-@rectified_sparse_attention_op.register_fake
-def _(q, k, v, num_text_tokens, block, top_k_fraction, weight_threshold, adjacency_radius,
-      force_text_blocks, variant):
-    return _out_like(q, k, v)
+_load()
 
 
-@torch.library.custom_op(f"{_LIB_NS}::rectified_sparse_attention_status", mutates_args=())
-def rectified_sparse_attention_status_op(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
-                                         num_text_tokens: int, block: int, top_k_fraction: float,
-                                         weight_threshold: float, adjacency_radius: int,
-                                         force_text_blocks: bool, variant: str
-                                         ) -> tuple[torch.Tensor, torch.Tensor]:
-    """Non-synchronising form: returns (out, status int32[4]) with the device
-    flags of this call; ``raise_for_status(status)`` raises the reference
-    exception when the caller next synchronises."""
-    from .pipeline import new_status
-    status = new_status(q.device)
-    out = _impl(q, k, v, num_text_tokens=num_text_tokens, block=block, top_k_fraction=top_k_fraction,
-                weight_threshold=weight_threshold, adjacency_radius=adjacency_radius,
-                force_text_blocks=force_text_blocks, variant=variant, check_status=False, status=status)
-    return out, status
+def typed_error(exc: RuntimeError) -> Exception:
+    """The reference exception class an operator error names, else the error."""
+    msg = str(exc)
+    for line in msg.splitlines():
+        name, sep, rest = line.partition(": ")
+        cls = getattr(errors, name.strip(), None) if sep else None
+        if isinstance(cls, type) and issubclass(cls, errors.RectAttnError):
+            return cls(rest)
+    return exc
 
 
-@rectified_sparse_attention_status_op.register_fake
-def _(q, k, v, num_text_tokens, block, top_k_fraction, weight_threshold, adjacency_radius,
-      force_text_blocks, variant):
-    return _out_like(q, k, v), q.new_empty(4, dtype=torch.int32)
+def rectified_sparse_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, num_text_tokens: int,
+                               block: int = 128, top_k_fraction: float = 0.1, weight_threshold: float = 0.0,
+                               adjacency_radius: int = 0, force_text_blocks: bool = False,
+                               variant: str = "sparse-rectified") -> torch.Tensor:
+    """``torch.ops.rsa_b200.rectified_sparse_attention`` with the reference's
+    exception classes."""
+    try:
+        return torch.ops.rsa_b200.rectified_sparse_attention(q, k, v, num_text_tokens, block, top_k_fraction,
+                                                             weight_threshold, adjacency_radius,
+                                                             force_text_blocks, variant)
+    except RuntimeError as exc:
+        raise typed_error(exc) from exc

@@ -64,7 +64,7 @@ def test_device_call_raises_by_default_and_accumulates_without_sync():
 
 
 def test_torch_op_status_output():
-    from paper_2511_19835_b200 import ops  # noqa: F401
+    from paper_2511_19835_b200 import ops
     q, k, v = qkv(2, 64 * 10, 30, 64)
     v[0, 1, 3, 3] = float("nan")
     out, status = torch.ops.rsa_b200.rectified_sparse_attention_status(q, k, v, 30, 64, 0.1, 0.0, 0, False,
@@ -72,8 +72,12 @@ def test_torch_op_status_output():
     assert out.shape == q.shape
     with pytest.raises(rsa.ShapeError):
         rsa.raise_for_status(status)
-    with pytest.raises(rsa.ShapeError):
+    # the C++ operator raises RuntimeError naming the reference class; the
+    # ops.py wrapper re-raises that class
+    with pytest.raises(RuntimeError, match="^ShapeError: "):
         torch.ops.rsa_b200.rectified_sparse_attention(q, k, v, 30, 64, 0.1, 0.0, 0, False, "sparse-rectified")
+    with pytest.raises(rsa.ShapeError):
+        ops.rectified_sparse_attention(q, k, v, 30, 64, 0.1, 0.0, 0, False, "sparse-rectified")
 
 
 @pytest.mark.timeout(180)

@@ -134,6 +134,25 @@ def test_torch_library_op():
     assert_bf16_close(out[0], np.concatenate([ref["o_video"], ref["o_text"]]), "torch.ops")
 
 
+def test_torch_library_op_equals_the_c_abi_call():
+    """The C++ TORCH_LIBRARY op (csrc/torch_ops.cpp) and the ctypes C-ABI API
+    run the same kernels: bitwise equal outputs, contiguous and through the
+    no-copy strided path (a [B, T, H, d] view and fused-qkv slices)."""
+    from paper_2511_19835_b200 import ops  # noqa: F401
+    g = torch.Generator().manual_seed(5)
+    qkv = torch.randn(1, 128 * 9 + 64, 3, 4, 128, generator=g).to(torch.bfloat16).cuda()
+    q, k, v = (qkv[:, :, i].transpose(1, 2) for i in range(3))
+    kw = dict(num_text_tokens=64, block=128, top_k_fraction=0.25, weight_threshold=0.0, adjacency_radius=1,
+              force_text_blocks=True, variant="sparse-rectified")
+    want = rsa.rectified_sparse_attention(q.contiguous(), k.contiguous(), v.contiguous(), **kw)
+    for args in ((q, k, v), (q.contiguous(), k.contiguous(), v.contiguous())):
+        got = torch.ops.rsa_b200.rectified_sparse_attention(*args, *kw.values())
+        assert torch.equal(got, want)
+        got, status = torch.ops.rsa_b200.rectified_sparse_attention_status(*args, *kw.values())
+        assert torch.equal(got, want)
+        rsa.raise_for_status(status)
+
+
 def test_torch_library_opcheck_and_compile():
     """torch.library.opcheck (schema, fake/meta kernel vs the CUDA kernel,
     AOT dispatch) on the registered op, contiguous and strided inputs, and a
