@@ -1028,6 +1028,9 @@ struct CfgPair {
 #ifndef RSA_PAIR_KV_HINT
 #define RSA_PAIR_KV_HINT 0   // A/B: 1 = K/V loads without the evict_last L2 hint
 #endif
+#ifndef RSA_DESC_ADD
+#define RSA_DESC_ADD 1   // MMA descriptors as base + offset (1) or rebuilt per MMA (0, A/B)
+#endif
 #ifndef RSA_PAIR_L2PF
 #define RSA_PAIR_L2PF 0   // iterations ahead whose K/V blocks the producer prefetches into L2 (0: off)
 #endif
@@ -1187,12 +1190,23 @@ attn_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
       const uint32_t kb = ring_addr + (uint32_t)(st * C::STAGE);
       const uint32_t qb = q_addr + (uint32_t)(t * C::Q_BYTES);
       if (ptx::elect_one()) {
+#if RSA_DESC_ADD
+        // descriptors of the k-th K slice = base descriptor + (byte offset >> 4)
+        // (shared addresses < 2^18: the 14-bit address field never carries)
+        const uint64_t qd = ptx::sw128_desc(qb, 16, 1024), kd = ptx::sw128_desc(kb, 16, 1024);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint64_t off = (uint64_t)(((k / 4) * C::PANEL + (k % 4) * 32) >> 4);
+          ptx::mma_ss(tmem + (uint32_t)(t * 128), qd + off, kd + off, C::IDESC_S, k > 0);
+        }
+#else
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t off = (uint32_t)((k / 4) * C::PANEL + (k % 4) * 32);
           ptx::mma_ss(tmem + (uint32_t)(t * 128), ptx::sw128_desc(qb + off, 16, 1024),
                       ptx::sw128_desc(kb + off, 16, 1024), C::IDESC_S, k > 0);
         }
+#endif
         ptx::tc_commit(kv_empty + st);   // K block read
         ptx::tc_commit(s_full + t);
       }
@@ -1213,10 +1227,18 @@ attn_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
       tr += 3;
       const uint32_t vb = ring_addr + (uint32_t)(st * C::STAGE);
       if (ptx::elect_one()) {
+#if RSA_DESC_ADD
+        const uint64_t vd = ptx::sw128_desc(vb, C::PANEL, 1024);
+#pragma unroll
+        for (int k = 0; k < 128 / 16; ++k)
+          ptx::mma_ts(tmem + 256u + (uint32_t)(t * 128), tmem + (uint32_t)(t * 128) + k * 8,
+                      vd + (uint64_t)(k * (2048 >> 4)), C::IDESC_O, (!first || k > 0) ? 1u : 0u);
+#else
 #pragma unroll
         for (int k = 0; k < 128 / 16; ++k)
           ptx::mma_ts(tmem + 256u + (uint32_t)(t * 128), tmem + (uint32_t)(t * 128) + k * 8,
                       ptx::sw128_desc(vb + k * 2048, C::PANEL, 1024), C::IDESC_O, (!first || k > 0) ? 1u : 0u);
+#endif
         ptx::tc_commit(kv_empty + st);   // V block read
         if (last) ptx::tc_commit(o_full + t);
       }
