@@ -1028,6 +1028,9 @@ struct CfgPair {
 #ifndef RSA_PAIR_KV_HINT
 #define RSA_PAIR_KV_HINT 0   // A/B: 1 = K/V loads without the evict_last L2 hint
 #endif
+#ifndef RSA_PAIR_FASTLOOP
+#define RSA_PAIR_FASTLOOP 1   // steady-state MMA loop without first/last flags (0: one general loop, A/B)
+#endif
 #ifndef RSA_DESC_ADD
 #define RSA_DESC_ADD 1   // MMA descriptors as base + offset (1) or rebuilt per MMA (0, A/B)
 #endif
@@ -1252,14 +1255,31 @@ attn_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
       const int c1 = e1 ? (int)decode_tile(P, b1).count : 0;
       const int cmax = c0 > c1 ? c0 : c1;
       if (c0 > 0) issue_s(0, true);
-      for (int j = 0; j <= cmax; ++j) {
+      auto general = [&](int j) {
         if (j >= 1 && j <= c1) issue_pv(1, j == 1, j == c1);
         if (j < c1) issue_s(1, j == 0);
         if (j < c0) {
           issue_pv(0, j == 0, j == c0 - 1);
           if (j + 1 < c0) issue_s(0, false);
         }
+      };
+#if RSA_PAIR_FASTLOOP
+      // steady state (2 <= j < min(c1, c0 - 1)): all four groups, no first /
+      // last flags -- a straight-line body with compile-time arguments keeps the
+      // MMA thread's work between groups short (it sits on both tiles' chains)
+      const int fast_end = c1 < c0 - 1 ? c1 : c0 - 1;
+      int j = 0;
+      for (; j <= cmax && j < 2; ++j) general(j);
+      for (; j < fast_end; ++j) {
+        issue_pv(1, false, false);
+        issue_s(1, false);
+        issue_pv(0, false, false);
+        issue_s(0, false);
       }
+      for (; j <= cmax; ++j) general(j);
+#else
+      for (int j = 0; j <= cmax; ++j) general(j);
+#endif
       // a tile with an empty kv list (the C ABI's mask seam flags it as
       // RSA_ERR_EMPTY_ROW): its group still loaded Q and releases one P phase
       // after its previous epilogue; answer with the o_full phase (so o_full
