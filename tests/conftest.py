@@ -10,7 +10,20 @@ if str(ROOT) not in sys.path:
     sys.path.insert(0, str(ROOT))
 
 
+def _ensure_built():
+    """The native libraries are build products (git-ignored): build them once
+    if a fresh checkout runs the tests before ``__graft_entry__.build()``."""
+    pkg = ROOT / "paper_2511_19835_b200"
+    if (pkg / "librsa_b200.so").exists() and (pkg / "librsa_b200_torch.so").exists():
+        return
+    import shutil
+    if shutil.which("nvcc") or Path("/usr/local/cuda/bin/nvcc").exists():
+        from paper_2511_19835_b200.build import build
+        build(verbose=False)
+
+
 def pytest_configure(config):
+    _ensure_built()
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) and the built CUDA library")
     config.addinivalue_line("markers", "slow: long-running CPU test")
 
