@@ -382,9 +382,10 @@ def _measure(torch, nat, lib, shape, conf, q, k, v, out, ws, steps, warm):
     import ctypes as C_
     from paper_2511_19835_b200.pipeline import _ptr, _stream
     st, sp = torch.cuda.current_stream(), _stream()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-    rows = []
-    for i in range(warm + steps):
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(warm + steps)]
+    # back-to-back calls, one synchronisation: the host enqueues ahead of the
+    # GPU, so no event pair brackets host-side launch latency
+    for ev in evs:
         ev[0].record(st)
         nat.check(lib.rsa_pool(C_.byref(shape), _ptr(q), _ptr(k), _ptr(v), _ptr(ws), sp))
         ev[1].record(st)
@@ -393,10 +394,9 @@ def _measure(torch, nat, lib, shape, conf, q, k, v, out, ws, steps, warm):
         nat.check(lib.rsa_attention(C_.byref(shape), C_.byref(conf), _ptr(q), _ptr(k), _ptr(v), _ptr(out),
                                     None, _ptr(ws), sp))
         ev[3].record(st)
-        torch.cuda.synchronize()
-        if i >= warm:
-            rows.append([ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3]),
-                         ev[0].elapsed_time(ev[3])])
+    torch.cuda.synchronize()
+    rows = [[ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3]),
+             ev[0].elapsed_time(ev[3])] for ev in evs[warm:]]
     nat.check(lib.rsa_check_device_status(_ptr(ws), sp))
     med = [statistics.median(r[j] for r in rows) for j in range(4)]
     return {"pool": med[0], "select": med[1], "attention": med[2], "call": med[3]}
@@ -575,13 +575,20 @@ def run_ours(args):
             step(record=False)
         t1.record(st)
         torch.cuda.synchronize()
-        # per-kernel split, measured on the launching stream in separate steps
-        for _ in range(max(2, min(args.steps, 5))):
+        # per-kernel split, measured on the launching stream over back-to-back
+        # steps (one unrecorded step first, so the host enqueues ahead of the GPU
+        # and no event pair brackets host-side launch latency), synchronised once
+        n_split = max(2, min(args.steps, 5))
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(n_split)]
+        step(record=False)
+        for i in range(n_split):
+            ev[:] = evs[i]
             step(record=True)
-            torch.cuda.synchronize()
-            per_stage["pool"].append(ev[0].elapsed_time(ev[1]))
-            per_stage["select"].append(ev[1].elapsed_time(ev[2]))
-            per_stage["attention"].append(ev[2].elapsed_time(ev[3]))
+        torch.cuda.synchronize()
+        for e4 in evs:
+            per_stage["pool"].append(e4[0].elapsed_time(e4[1]))
+            per_stage["select"].append(e4[1].elapsed_time(e4[2]))
+            per_stage["attention"].append(e4[2].elapsed_time(e4[3]))
     if world > 1:
         dist.barrier()
     total_ms = t0.elapsed_time(t1)
