@@ -1028,6 +1028,9 @@ struct CfgPair {
 #ifndef RSA_PAIR_KV_HINT
 #define RSA_PAIR_KV_HINT 0   // A/B: 1 = K/V loads without the evict_last L2 hint
 #endif
+#ifndef RSA_TMEM_ZERO
+#define RSA_TMEM_ZERO 1   // paired-tile kernel: TMEM base as the constant 0 (checked); 0 = read it (A/B)
+#endif
 #ifndef RSA_PAIR_FASTLOOP
 #define RSA_PAIR_FASTLOOP 1   // steady-state MMA loop without first/last flags (0: one general loop, A/B)
 #endif
@@ -1079,7 +1082,16 @@ attn_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
+#if RSA_TMEM_ZERO
+  // A CTA's only allocation of all 512 columns starts at lane 0, column 0: the
+  // TMEM base is the constant 0, so every tcgen05 address below is a
+  // compile-time constant (no vector -> uniform register moves on the MMA
+  // thread between groups).  Checked once.
+  if (*tmem_slot != 0u) __trap();
+  constexpr uint32_t tmem = 0u;
+#else
   const uint32_t tmem = *tmem_slot;
+#endif
 
   if (warp < 4) {
     ptx::regs_dec<80>();

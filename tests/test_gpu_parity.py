@@ -153,6 +153,31 @@ def test_torch_library_op_equals_the_c_abi_call():
         rsa.raise_for_status(status)
 
 
+def test_torch_library_op_fp32_and_small_head_dim():
+    """The C++ op on the other shape classes: fp32 (CUDA-core K3, contiguous
+    copy of a strided input) against the fp64 oracle, and a d = B = 64 bf16
+    [B, T, H, d] view (persistent tcgen05 K3, no-copy path) against the
+    contiguous call, bitwise."""
+    from paper_2511_19835_b200 import ops  # noqa: F401
+    qv, qt, k, v = O.gen_synthetic(7, 64 * 12, 40, 64, 64, (1, 12, 64), 1.0, 2.0, 0.3)
+    q32 = torch.from_numpy(np.concatenate([qv, qt]).astype(np.float32)).cuda()[None]
+    k32 = torch.from_numpy(k.astype(np.float32)).cuda()[None]
+    v32 = torch.from_numpy(v.astype(np.float32)).cuda()[None]
+    out = torch.ops.rsa_b200.rectified_sparse_attention(q32, k32, v32, 40, 64, 0.25, 0.0, 0, False,
+                                                        "sparse-rectified")
+    ref = O.pipeline(qv.astype(np.float64), qt.astype(np.float64), k.astype(np.float64), v.astype(np.float64),
+                     64, 0.25, 0.0, 0, False, "sparse-rectified")
+    np.testing.assert_allclose(out[0].cpu().numpy(), np.concatenate([ref["o_video"], ref["o_text"]]),
+                               atol=1e-5, rtol=0)
+    g = torch.Generator().manual_seed(9)
+    x = [torch.randn(2, 64 * 10 + 30, 3, 64, generator=g).to(torch.bfloat16).cuda() for _ in range(3)]
+    qs, ks, vs = (t.transpose(1, 2) for t in x)          # [B, H, T, d] views
+    got = torch.ops.rsa_b200.rectified_sparse_attention(qs, ks, vs, 30, 64, 0.2, 0.0, 0, False, "sparse-rectified")
+    want = torch.ops.rsa_b200.rectified_sparse_attention(qs.contiguous(), ks.contiguous(), vs.contiguous(), 30, 64,
+                                                         0.2, 0.0, 0, False, "sparse-rectified")
+    assert got.stride() == qs.stride() and torch.equal(got, want)
+
+
 def test_torch_library_opcheck_and_compile():
     """torch.library.opcheck (schema, fake/meta kernel vs the CUDA kernel,
     AOT dispatch) on the registered op, contiguous and strided inputs, and a
