@@ -1026,7 +1026,7 @@ struct CfgPair {
                           // rounds: -1.9 % K3), 2 the softmax S waits (no gain)
 #endif
 #ifndef RSA_PAIR_KV_HINT
-#define RSA_PAIR_KV_HINT 0   // A/B: 1 = K/V loads without the evict_last L2 hint
+#define RSA_PAIR_KV_HINT 0   // A/B: 1 = K/V loads without the evict_last L2 hint; 2 = only K, 3 = only V evict_last
 #endif
 #ifndef RSA_TMEM_ZERO
 #define RSA_TMEM_ZERO 1   // paired-tile kernel: TMEM base as the constant 0 (checked); 0 = read it (A/B)
@@ -1099,6 +1099,8 @@ attn_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     // ===================== TMA producer: K/V blocks in MMA order =====================
       ptx::prefetch_tmap(&tm_k);
       ptx::prefetch_tmap(&tm_v);
+      const uint64_t normal = ptx::policy_evict_normal();
+      (void)normal;
 #if RSA_PAIR_KV_HINT == 1
       const uint64_t keep = ptx::policy_evict_normal();
 #else
@@ -1168,7 +1170,8 @@ attn_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             const int row0 = (int)kv_row0(g, m), hh = tt ? h1 : h0;
 #pragma unroll
             for (int p = 0; p < 2; ++p)
-              tma_rows(dst + p * C::PANEL, tmap, kv_full + st, 64 * p, row0, hh, g, keep);
+              tma_rows(dst + p * C::PANEL, tmap, kv_full + st, 64 * p, row0, hh, g,
+                       RSA_PAIR_KV_HINT >= 2 ? ((q4 & 1) == (RSA_PAIR_KV_HINT - 2) ? keep : normal) : keep);
             if (++st == C::NST) { st = 0; ph ^= 1; }
           }
           m1_prev = m1;
