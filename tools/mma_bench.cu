@@ -42,6 +42,18 @@ __global__ void __launch_bounds__(128, 1) bench(long long* out, int iters) {
       // MN == 3: K-major only, alternating accumulators every 8; MN == 4: MN-major only, alternating;
       // MN == 5: alternating majorness, same accumulator and same A
       const bool mn = MN == 1 || MN == 4 || ((MN == 2 || MN == 5) && ((i / 8) & 1));
+      if (MN == 6) {
+        // the 64-key sub-step sequence: 8 x S_half (TS, N = 64, K-major B, acc at col 0)
+        // then 4 x PV_half (TS, N = 128, MN-major B, K = 64 keys, acc at col 256), repeated
+        const int ph = i % 12;
+        if (ph < 8) {
+          mma_ts(tmem, tmem + 384 + ph * 8, sw128_desc(b_addr + (ph % 4) * 32, 16, 1024), idesc_bf16(128, 64, false), 1);
+        } else {
+          mma_ts(tmem + 256u, tmem + 448 + (ph - 8) * 8, sw128_desc(b_addr + (ph - 8) * 2048, 16384, 1024),
+                 idesc_bf16(128, 128, true), 1);
+        }
+        continue;
+      }
       if (MN >= 3) {
         const uint64_t bb = mn ? sw128_desc(b_addr + (i % 8) * 2048, 16384, 1024) : sw128_desc(b_addr + (i % 4) * 32, 16, 1024);
         const uint32_t acc = (MN == 5) ? tmem : tmem + (((i / 8) & 1) ? 256u : 0u);
@@ -265,5 +277,7 @@ int main() {
   run<128, true, 1, 0, 3>("TS K-major, 2 accs alt/8", sms);
   run<128, true, 1, 0, 4>("TS MN-major, 2 accs alt/8", sms);
   run<128, true, 1, 0, 5>("TS K/MN alt/8 same acc", sms);
+  run<64, true, 1>("TS N=64 K-major", sms);
+  run<64, true, 1, 0, 6>("64-key sub-step: 8 S N=64 + 4 PV N=128 (ideal/MMA: 8x32+4x64 over 12)", sms);
   return 0;
 }
